@@ -1,0 +1,313 @@
+"""Benchmark: CCD queries/sec (FP64, delta=1e-6) on B200, + FP64 roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1] [--queries Q]
+
+One step = one batched solve of this rank's queries of the workload (default
+BASELINE config 1: mixed VF/EE, half planted collisions, delta=1e-6,
+m_I=1e6, d=0, t_max=1; Q = 10^6 queries per GPU, weak scaling: rank r solves
+queries [r*Q, (r+1)*Q) of the index-addressable synthetic stream).  Inputs
+(192 MB per 10^6 queries) exceed the 126 MB L2, so no flush is needed.
+
+value  = device-timed throughput, inputs resident in HBM, CUDA events on the
+         launching stream, barrier + synchronize on both sides, max over ranks.
+e2e    = the same through the public API with pinned HOST inputs: H2D of
+         points + kind and D2H of status + toi inside the timed region.
+roofline = algorithmic FP64 flops (per query P_kind + checks *
+         F_kind, F_VF = 200, F_EE = 174, P_VF = 248, P_EE = 222, checks = the
+         reference's own count, which the kernel reproduces exactly) / the
+         solve's average duration, vs the DFMA peak measured on this box by
+         libtccd_probe.so (FMA-counted; an FMA-free kernel is capped at 0.5).
+cpu_baseline = the C restatement of the reference (oracle/, kind "port") on
+         all host cores, rank 0 at N=1, on a bounded sample.
+--impl reference: that CPU path alone, same metric/config (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+F_CHECK = {0: 200, 1: 174}
+P_QUERY = {0: 248, 1: 222}
+METRIC = "CCD queries/sec (FP64, delta=1e-6) at 1/2/4/8 B200; % of FP64 roofline"
+
+
+def algorithmic_flops(kind: np.ndarray, checks: np.ndarray) -> float:
+    vf = kind == 0
+    return float(np.sum(np.where(vf, P_QUERY[0] + checks * F_CHECK[0],
+                                 P_QUERY[1] + checks * F_CHECK[1]).astype(np.float64)))
+
+
+def workload_desc(cfg: int, q: int) -> dict:
+    from paper_2009_13349_b200 import workloads as W
+    names = {
+        0: "config0: vertex-face, U[0,1]^3 + U[-0.5,0.5]^3 motion",
+        1: "config1: 50% VF / 50% EE, half planted exact roots, half config-0 random",
+        2: "config2: degenerate lattice families, delta in {1e-4,1e-6,1e-8}, m_I in {1e3,1e6}",
+        3: "config3: simulation-shaped, 80% VF / 20% EE, edge 1e-2, offsets N(0,1e-3)/N(0,5e-3)",
+    }
+    return {"workload": names.get(cfg, W.CONFIGS[cfg]["name"]), "baseline_config": cfg,
+            "queries_per_gpu": q, "delta": 1e-6 if cfg != 2 else "per-query",
+            "max_checks": 1_000_000 if cfg != 2 else "per-query", "separation": 0.0,
+            "t_max": 1.0, "seed": f"PCG64(SeedSequence([{W.SEED_BASE}+{cfg}, block]))",
+            "l2": "inputs > 126 MB L2 per step (no flush needed)" if q * 192 > 126e6
+            else "inputs < L2; L2 flushed between steps"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons while the timed region runs."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout
+                    for line in out.strip().splitlines():
+                        self.rows.append([c.strip() for c in line.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self) -> dict:
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 9:
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def fp64_peaks() -> dict:
+    so = os.path.join(ROOT, "paper_2009_13349_b200", "libtccd_probe.so")
+    L = ctypes.CDLL(so)
+    L.tccd_probe_dfma_tflops.restype = ctypes.c_double
+    L.tccd_probe_dfma_tflops.argtypes = [ctypes.c_int, ctypes.c_int]
+    L.tccd_probe_dadd_tflops.restype = ctypes.c_double
+    L.tccd_probe_dadd_tflops.argtypes = [ctypes.c_int, ctypes.c_int]
+    return {"dfma_tflops": L.tccd_probe_dfma_tflops(20000, 5),
+            "dadd_tflops": L.tccd_probe_dadd_tflops(20000, 5)}
+
+
+def cpu_sample(cfg: int, start: int, target_s: float, threads: int, chunk: int = 20000):
+    """Run the oracle port on consecutive chunks until ~target_s elapsed."""
+    import oracle
+    from paper_2009_13349_b200 import workloads as W
+    done, t_cpu, lo = 0, 0.0, start
+    while t_cpu < target_s:
+        w = W.generate(cfg, lo, chunk)
+        t0 = time.perf_counter()
+        oracle.solve_batch(w.points, w.kind, w.delta, w.max_checks, w.separation, w.t_max,
+                           threads=threads)
+        t_cpu += time.perf_counter() - t0
+        done += w.n
+        lo += w.n
+    return done, t_cpu
+
+
+def run_reference(args, rank: int) -> None:
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    import oracle
+    oracle.lib()
+    per_step = max(args.ref_step_seconds, 0.5)
+    for _ in range(args.warmup):
+        cpu_sample(args.config, 0, 0.2, threads)
+    total_q, total_t = 0, 0.0
+    for s in range(args.steps):
+        q, t = cpu_sample(args.config, s * 200_000, per_step, threads)
+        total_q += q
+        total_t += t
+    value = total_q / total_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_desc(args.config, args.queries),
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads, "kind": "port",
+                         "sample": f"{total_q} queries of the workload stream in {args.steps} "
+                                   f"steps of ~{per_step:.0f}s (oracle/tccd_oracle.c, pthreads)"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--queries", type=int, default=1_000_000)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2009_13349_b200 import solve_batch
+    from paper_2009_13349_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    Q = args.queries
+    w = W.generate(args.config, rank * Q, Q)
+    pts_h = torch.from_numpy(w.points).pin_memory()
+    kind_h = torch.from_numpy(w.kind).pin_memory()
+    pts = pts_h.to(dev)
+    kind = kind_h.to(dev)
+    kw = {}
+    if args.config == 2:
+        kw = dict(delta=torch.from_numpy(w.delta).to(dev), max_checks=torch.from_numpy(w.max_checks).to(dev))
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return solve_batch(pts, kind, outputs=("status", "toi"), device=dev,
+                           raise_on_error=False, **kw)
+
+    # untimed: full outputs once, for the algorithmic work (checks) and hits
+    full = solve_batch(pts, kind, device=dev, stats=True, **kw)
+    checks = full["checks"].cpu().numpy()
+    hits = int((full["status"] == 1).sum().item())
+    evicted = int(full["stats"][0].item())
+    flops = algorithmic_flops(w.kind, checks)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    # end to end through the public API with pinned host buffers
+    barrier()
+    torch.cuda.synchronize(dev)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        r = solve_batch(pts_h, kind_h, outputs=("status", "toi"), device=dev,
+                        raise_on_error=False, **({k: v.cpu() for k, v in kw.items()}))
+    f1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.stop()
+    e2e_ms = f0.elapsed_time(f1) / args.steps
+
+    ms_max = max_over_ranks(ms)
+    e2e_ms_max = max_over_ranks(e2e_ms)
+    total_q = Q * world
+    value = total_q / (ms_max * 1e-3)
+    e2e_value = total_q / (e2e_ms_max * 1e-3)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = fp64_peaks()
+    achieved = flops / (ms * 1e-3) / 1e12
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        threads = len(os.sched_getaffinity(0))
+        nq, t = cpu_sample(args.config, 0, args.cpu_seconds, threads)
+        cpu = {"value": nq / t, "unit": "queries/s", "cores": threads, "kind": "port",
+               "sample": f"first {nq} queries of the same workload stream "
+                         f"(oracle/tccd_oracle.c on {threads} threads, {t:.1f}s)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_2009_13349_b200/workloads.py)",
+        "config": workload_desc(args.config, Q),
+        "e2e": {"value": e2e_value, "unit": "queries/s",
+                "h2d_bytes_per_step": int(pts_h.numel() * 8 + kind_h.numel()),
+                "d2h_bytes_per_step": int(Q * 9)},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peaks["dfma_tflops"],
+                     "unit": "TFLOP/s", "frac": achieved / peaks["dfma_tflops"],
+                     "traffic": None,
+                     "peak_source": "measured on this box: DFMA probe (libtccd_probe.so), FMA-counted",
+                     "fma_free_ceiling_tflops": peaks["dadd_tflops"],
+                     "flops_per_step": flops,
+                     "kernels": "light_kernel + heavy_kernel (one solve)"},
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "gpu_launches": 2 * args.steps * 2,
+        "workload_stats": {"hits": hits, "hit_rate": hits / Q, "mean_checks": float(checks.mean()),
+                           "max_checks": int(checks.max()), "evicted_to_block_engine": evicted},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/*
+ * tccd -- B200-native batched Tight-Inclusion CCD (arXiv 2009.13349).
+ *
+ * C-ABI of libtccd.so: plain pointers, sizes and a struct; no torch types.
+ * The library never allocates device memory on the batched path: the caller
+ * passes a workspace sized by tccd_workspace_bytes().  All device work is
+ * enqueued on the caller's stream (a cudaStream_t passed as void*).
+ *
+ * Reference interface each entry point replaces (paths under the reference
+ * repo):
+ *   tccd_solve_kernel  <- ccdkit._kernel.solve_kernel
+ *                         (pkg/src/ccdkit/_kernel.py:136-146, same argument
+ *                         list and the same 13-field result)
+ *   tccd_solve_batch   <- a loop of ccdkit.solver.solve(q, config)
+ *                         (pkg/src/ccdkit/solver.py:50-107) over a batch,
+ *                         including its filter resolution
+ *                         (_resolve_filters, solver.py:30-47 ->
+ *                         inclusion.compute_gamma / compute_filters,
+ *                         pkg/src/ccdkit/inclusion.py:85-122) and the
+ *                         SolverConfig validation (core.py:176-184)
+ *   tccd_workspace_bytes, tccd_error_string, tccd_abi_version: new (no
+ *                         reference counterpart; numba allocates internally)
+ */
+#ifndef TCCD_H
+#define TCCD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TCCD_ABI_VERSION 1
+
+/* Per-query status values written to tccd_batch.status. */
+#define TCCD_STATUS_FREE 0           /* certified collision free, toi = +inf   */
+#define TCCD_STATUS_HIT 1            /* collision, toi = witness t_lo          */
+#define TCCD_STATUS_ERR_SEPARATION 2 /* d >= gamma on an axis: the reference's
+                                        compute_filters ValueError
+                                        (inclusion.py:110-113)                 */
+#define TCCD_STATUS_ERR_NONFINITE 3  /* NaN/inf coordinate: Vec3 ValueError
+                                        (core.py:49-51)                        */
+#define TCCD_STATUS_ERR_PARAM 4      /* per-query delta/m_I/d/t_max/kind
+                                        outside SolverConfig's domain
+                                        (core.py:176-184)                      */
+
+/* Return codes. */
+#define TCCD_OK 0
+#define TCCD_E_NULL 1       /* a required pointer is NULL                     */
+#define TCCD_E_N 2          /* n < 0                                          */
+#define TCCD_E_DELTA 3      /* broadcast delta not > 0 and finite             */
+#define TCCD_E_MAXCHECKS 4  /* broadcast max_checks < 1                       */
+#define TCCD_E_TMAX 5       /* broadcast t_max not in (0, 1]                  */
+#define TCCD_E_SEPARATION 6 /* broadcast separation < 0 or non-finite         */
+#define TCCD_E_KIND 7       /* broadcast kind not 0/1                         */
+#define TCCD_E_WORKSPACE 8  /* workspace NULL or smaller than required        */
+#define TCCD_E_CUDA 9       /* a CUDA runtime call failed                     */
+#define TCCD_E_STRUCT 10    /* struct_size mismatch (ABI skew)                */
+#define TCCD_E_CAPACITY 11  /* max_checks_max exceeds what the layout indexes */
+
+/* flags */
+#define TCCD_FLAG_HEAVY_ONLY 1u /* route every query through the block-per-query
+                                   engine (testing / diagnostics)             */
+
+/*
+ * One batched solve.  All array pointers are DEVICE pointers.  For every
+ * per-query parameter, a NULL array means "use the broadcast *_all value".
+ *
+ * points: [n][8][3] f64, row-major: the 4 points at t0 in query order
+ *         (VF: p, v1, v2, v3; EE: p1, p2, p3, p4 -- core.py:86-89), then the
+ *         same 4 points at t1 (Query.all_coordinates(), core.py:114-116).
+ * kind:   [n] u8, 0 vertex-face, 1 edge-edge (QueryKind, core.py:75-79).
+ * eps:    NULL -> per-query gamma/eps computed on device exactly as
+ *         compute_gamma + compute_filters; else [n][3] caller filters
+ *         (a reused FilterEps, solver.py:30-47; not re-validated, like the
+ *         reference).
+ * Outputs: status and toi are required; the others may be NULL.
+ *         toi = +inf for status != HIT.  witness = [n][6]
+ *         (t_lo, t_hi, u_lo, u_hi, v_lo, v_hi).  tol = witness t width,
+ *         codom = witness hull width, checks = box classifications,
+ *         early = budget ended the search, level = witness BFS level.
+ */
+typedef struct tccd_batch {
+  uint32_t struct_size; /* = sizeof(tccd_batch)                       */
+  uint32_t flags;       /* TCCD_FLAG_*                                */
+  int64_t n;
+
+  const double *points;
+  const uint8_t *kind;
+  int32_t kind_all;
+  int32_t reserved0;
+  const double *delta;
+  double delta_all;
+  const int64_t *max_checks;
+  int64_t max_checks_all;
+  int64_t max_checks_max; /* upper bound over the batch; sizes the workspace */
+  const double *separation;
+  double separation_all;
+  const double *t_max;
+  double t_max_all;
+  const double *eps;
+
+  uint8_t *status;
+  double *toi;
+  double *tol;
+  double *codom;
+  int64_t *checks;
+  uint8_t *early;
+  double *witness;
+  int32_t *level;
+
+  void *workspace;
+  size_t workspace_bytes;
+  int32_t heavy_blocks; /* concurrent block-per-query solvers; 0 = default   */
+  int32_t device_sms;   /* SM count of the target device; 0 = query it      */
+  int64_t *stats;       /* optional device [4]: [0] queries moved to the
+                           block-per-query engine, [1] light-engine rounds,
+                           [2..3] reserved (written as 0)                  */
+} tccd_batch;
+
+/* Bytes of device workspace tccd_solve_batch needs for a batch of n queries
+ * whose largest check budget is max_checks_max, with heavy_blocks concurrent
+ * block-per-query solvers (0 = default for the current device). */
+size_t tccd_workspace_bytes(int64_t n, int64_t max_checks_max, int32_t heavy_blocks);
+
+/* Enqueue a batched solve on `stream` (cudaStream_t, NULL = legacy default).
+ * Returns TCCD_OK or a TCCD_E_* code; per-query failures go to status[]. */
+int tccd_solve_batch(const tccd_batch *batch, void *stream);
+
+/* Drop-in for _kernel.solve_kernel(s, e, kind, t_max, delta, max_checks,
+ * sep, ex, ey, ez) (_kernel.py:136): HOST pointers s[4][3], e[4][3];
+ * out13 receives (status, toi, tol, codom, checks, early, w_t0, w_t1, w_u0,
+ * w_u1, w_v0, w_v1, w_level) as doubles.  Synchronous; allocates its own
+ * device scratch (convenience path, not the throughput path). */
+int tccd_solve_kernel(const double *s, const double *e, int kind, double t_max,
+                      double delta, int64_t max_checks, double sep, double ex,
+                      double ey, double ez, double *out13);
+
+const char *tccd_error_string(int code);
+int tccd_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCCD_H */

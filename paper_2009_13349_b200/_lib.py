@@ -1,0 +1,115 @@
+"""ctypes binding of libtccd.so (include/tccd.h).
+
+The shared library is built in-tree (``make -C paper_2009_13349_b200/csrc``
+or ``__graft_entry__.build()``).  There is no fallback: if the library is
+missing or fails to load, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtccd.so")
+
+ABI_VERSION = 1
+FLAG_HEAVY_ONLY = 1
+
+STATUS_FREE = 0
+STATUS_HIT = 1
+STATUS_ERR_SEPARATION = 2
+STATUS_ERR_NONFINITE = 3
+STATUS_ERR_PARAM = 4
+
+_vp = ctypes.c_void_p
+
+
+class TccdBatch(ctypes.Structure):
+    """Mirror of ``struct tccd_batch`` (include/tccd.h)."""
+
+    _fields_ = [
+        ("struct_size", ctypes.c_uint32),
+        ("flags", ctypes.c_uint32),
+        ("n", ctypes.c_int64),
+        ("points", _vp),
+        ("kind", _vp),
+        ("kind_all", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
+        ("delta", _vp),
+        ("delta_all", ctypes.c_double),
+        ("max_checks", _vp),
+        ("max_checks_all", ctypes.c_int64),
+        ("max_checks_max", ctypes.c_int64),
+        ("separation", _vp),
+        ("separation_all", ctypes.c_double),
+        ("t_max", _vp),
+        ("t_max_all", ctypes.c_double),
+        ("eps", _vp),
+        ("status", _vp),
+        ("toi", _vp),
+        ("tol", _vp),
+        ("codom", _vp),
+        ("checks", _vp),
+        ("early", _vp),
+        ("witness", _vp),
+        ("level", _vp),
+        ("workspace", _vp),
+        ("workspace_bytes", ctypes.c_size_t),
+        ("heavy_blocks", ctypes.c_int32),
+        ("device_sms", ctypes.c_int32),
+        ("stats", _vp),
+    ]
+
+
+EXPORTS = (
+    "tccd_abi_version",
+    "tccd_error_string",
+    "tccd_workspace_bytes",
+    "tccd_solve_batch",
+    "tccd_solve_kernel",
+)
+
+_lib = None
+
+
+class TccdError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: tccd error {code}: {error_string(code)}")
+        self.code = code
+
+
+def lib() -> ctypes.CDLL:
+    """Load libtccd.so (raises if it is missing: there is no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} not built; run `make -C {_HERE}/csrc` or __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        L.tccd_abi_version.restype = ctypes.c_int
+        L.tccd_abi_version.argtypes = []
+        L.tccd_error_string.restype = ctypes.c_char_p
+        L.tccd_error_string.argtypes = [ctypes.c_int]
+        L.tccd_workspace_bytes.restype = ctypes.c_size_t
+        L.tccd_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32]
+        L.tccd_solve_batch.restype = ctypes.c_int
+        L.tccd_solve_batch.argtypes = [ctypes.POINTER(TccdBatch), _vp]
+        L.tccd_solve_kernel.restype = ctypes.c_int
+        L.tccd_solve_kernel.argtypes = [
+            _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int64,
+            ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, _vp]
+        v = L.tccd_abi_version()
+        if v != ABI_VERSION:
+            raise RuntimeError(f"libtccd ABI {v} != expected {ABI_VERSION}")
+        _lib = L
+    return _lib
+
+
+def error_string(code: int) -> str:
+    return lib().tccd_error_string(int(code)).decode()
+
+
+def check(code: int, where: str) -> None:
+    if code != 0:
+        raise TccdError(code, where)

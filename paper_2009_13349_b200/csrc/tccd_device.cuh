@@ -1,0 +1,256 @@
+// Device-side numerics of the inclusion-based CCD root finder.
+//
+// Every function here reproduces the reference's binary64 operation order
+// exactly (the filter constants were derived for it: pkg/src/ccdkit/core.py:
+// 19-23, inclusion.py:8-15).  The translation unit is compiled with
+// --fmad=false so no multiply/add pair is contracted into a DFMA; common
+// subexpressions are shared only where the shared value is bit-identical to
+// what the reference recomputes (same operands, same single operation).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tccd {
+
+constexpr int kDisjoint = 0;    // _kernel.py:36
+constexpr int kIntersects = 1;  // _kernel.py:37
+constexpr int kContained = 2;   // _kernel.py:38
+
+// per-query status (include/tccd.h)
+constexpr uint8_t kFree = 0, kHit = 1, kErrSeparation = 2, kErrNonfinite = 3, kErrParam = 4;
+
+// inclusion.py:35-38
+constexpr double kCoefVF = 6.661338147750939e-15;
+constexpr double kCoefEE = 6.217248937900877e-15;
+constexpr double kCoefVFd = 7.549516567451064e-15;
+constexpr double kCoefEEd = 7.105427357601002e-15;
+
+struct Box {
+  double t0, t1, u0, u1, v0, v1;
+};
+
+// Per-query constants every box check needs.  Points are point-major:
+// P[3*k + ax] is point k at t0 (k = 0..3), P[12 + 3*k + ax] at t1.
+struct QueryParams {
+  double eps[3];
+  double kap[3];
+  double sep, delta, t_max;
+  long long max_checks;
+  int kind;
+};
+
+// F on one axis at the 4 (u, v) corners for one time value; the lerped
+// point coordinates a..d are (1 - t) * s + t * e (core.py:221-222).
+// VF: p - (((1 - u) - v) * v1 + u * v2 + v * v3)        (core.py:236)
+// EE: ((1 - u) * p1 + u * p2) - ((1 - v) * p3 + v * p4)  (core.py:254)
+struct CornerWeights {
+  double u0, u1, v0, v1;
+  double omu0, omu1, omv0, omv1;  // 1 - u, 1 - v
+  double w00, w01, w10, w11;      // (1 - u) - v   (VF only)
+};
+
+__device__ __forceinline__ CornerWeights corner_weights(const Box& b) {
+  CornerWeights w;
+  w.u0 = b.u0; w.u1 = b.u1; w.v0 = b.v0; w.v1 = b.v1;
+  w.omu0 = 1.0 - b.u0; w.omu1 = 1.0 - b.u1;
+  w.omv0 = 1.0 - b.v0; w.omv1 = 1.0 - b.v1;
+  w.w00 = w.omu0 - b.v0; w.w01 = w.omu0 - b.v1;
+  w.w10 = w.omu1 - b.v0; w.w11 = w.omu1 - b.v1;
+  return w;
+}
+
+template <int KIND>
+__device__ __forceinline__ void corners_at_t(double a, double b, double c, double d,
+                                             const CornerWeights& w, double& mn, double& mx) {
+  double f00, f01, f10, f11;
+  if (KIND == 0) {
+    const double cu0 = w.u0 * c, cu1 = w.u1 * c, dv0 = w.v0 * d, dv1 = w.v1 * d;
+    f00 = a - ((w.w00 * b + cu0) + dv0);
+    f01 = a - ((w.w01 * b + cu0) + dv1);
+    f10 = a - ((w.w10 * b + cu1) + dv0);
+    f11 = a - ((w.w11 * b + cu1) + dv1);
+  } else {
+    const double l0 = w.omu0 * a + w.u0 * b, l1 = w.omu1 * a + w.u1 * b;
+    const double r0 = w.omv0 * c + w.v0 * d, r1 = w.omv1 * c + w.v1 * d;
+    f00 = l0 - r0; f01 = l0 - r1; f10 = l1 - r0; f11 = l1 - r1;
+  }
+  // min/max of binary64 values: order-free, and +-0 never changes a
+  // classification or a width, so fmin/fmax are exact.
+  mn = fmin(fmin(mn, fmin(f00, f01)), fmin(f10, f11));
+  mx = fmax(fmax(mx, fmax(f00, f01)), fmax(f10, f11));
+}
+
+// _kernel._hull_axis (_kernel.py:44-67) for one axis.
+template <int KIND, typename PtrT>
+__device__ __forceinline__ void hull_axis(PtrT P, int ax, double t0, double omt0, double t1,
+                                          double omt1, const CornerWeights& w, double& mn,
+                                          double& mx) {
+  const double s0 = P[ax], s1 = P[3 + ax], s2 = P[6 + ax], s3 = P[9 + ax];
+  const double e0 = P[12 + ax], e1 = P[15 + ax], e2 = P[18 + ax], e3 = P[21 + ax];
+  mn = __longlong_as_double(0x7ff0000000000000LL);   // +inf
+  mx = __longlong_as_double((long long)0xfff0000000000000ULL);  // -inf
+  corners_at_t<KIND>(omt0 * s0 + t0 * e0, omt0 * s1 + t0 * e1, omt0 * s2 + t0 * e2,
+                     omt0 * s3 + t0 * e3, w, mn, mx);
+  corners_at_t<KIND>(omt1 * s0 + t1 * e0, omt1 * s1 + t1 * e1, omt1 * s2 + t1 * e2,
+                     omt1 * s3 + t1 * e3, w, mn, mx);
+}
+
+// _kernel._classify (_kernel.py:71-94): axes x, y, z with an early return
+// at the first separated axis; hull enlarged by sep before comparing; wb is
+// the raw (unenlarged) max width, 0 when disjoint.
+template <int KIND, typename PtrT>
+__device__ __forceinline__ int classify_k(PtrT P, const Box& b, const double* eps, double sep,
+                                          double& wb) {
+  const CornerWeights w = corner_weights(b);
+  const double omt0 = 1.0 - b.t0, omt1 = 1.0 - b.t1;
+  bool contained = true;
+  double width = 0.0;
+#pragma unroll 1
+  for (int ax = 0; ax < 3; ++ax) {
+    double mn, mx;
+    hull_axis<KIND>(P, ax, b.t0, omt0, b.t1, omt1, w, mn, mx);
+    const double e = eps[ax];
+    const double lo = mn - sep, hi = mx + sep;
+    if (lo > e || hi < -e) {
+      wb = 0.0;
+      return kDisjoint;
+    }
+    if (!(lo >= -e && hi <= e)) contained = false;
+    const double d = mx - mn;
+    if (d > width) width = d;
+  }
+  wb = width;
+  return contained ? kContained : kIntersects;
+}
+
+template <typename PtrT>
+__device__ __forceinline__ int classify(PtrT P, int kind, const Box& b, const double* eps,
+                                        double sep, double& wb) {
+  return kind == 0 ? classify_k<0>(P, b, eps, sep, wb) : classify_k<1>(P, b, eps, sep, wb);
+}
+
+// _kernel._kappas (_kernel.py:98-132): 3 * max |F(corner + stride) - F(corner)|
+// over the domain [0, t_max] x [0,1]^2, strides t=4, u=2, v=1.
+template <typename PtrT>
+__device__ __forceinline__ void kappas(PtrT P, int kind, double t_max, double out[3]) {
+  double F[8][3];
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double t = it ? t_max : 0.0;
+    const double omt = 1.0 - t;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const double a = omt * P[ax] + t * P[12 + ax];
+      const double b = omt * P[3 + ax] + t * P[15 + ax];
+      const double c = omt * P[6 + ax] + t * P[18 + ax];
+      const double d = omt * P[9 + ax] + t * P[21 + ax];
+#pragma unroll
+      for (int iu = 0; iu < 2; ++iu)
+#pragma unroll
+        for (int iv = 0; iv < 2; ++iv) {
+          const double u = iu ? 1.0 : 0.0, v = iv ? 1.0 : 0.0;
+          double val;
+          if (kind == 0) val = a - ((1.0 - u - v) * b + u * c + v * d);
+          else val = ((1.0 - u) * a + u * b) - ((1.0 - v) * c + v * d);
+          F[4 * it + 2 * iu + iv][ax] = val;
+        }
+    }
+  }
+  const int strides[3] = {4, 2, 1};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double best = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i & strides[k]) continue;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        const double d = fabs(F[i + strides[k]][ax] - F[i][ax]);
+        if (d > best) best = d;
+      }
+    }
+    out[k] = 3.0 * best;
+  }
+}
+
+// compute_gamma + compute_filters (inclusion.py:85-122).  Returns kHit on
+// success, else the per-query error status.
+template <typename PtrT>
+__device__ __forceinline__ uint8_t filters(PtrT P, int kind, double sep, double eps[3]) {
+  double g[3] = {0.0, 0.0, 0.0};
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const double x = P[3 * i + ax];
+      finite &= isfinite(x);
+      g[ax] = fmax(g[ax], fabs(x));
+    }
+  if (!finite) return kErrNonfinite;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) g[ax] = g[ax] > 1.0 ? g[ax] : 1.0;
+  double c;
+  if (sep > 0.0) {
+    if (!(sep < g[0] && sep < g[1] && sep < g[2])) return kErrSeparation;
+    c = kind == 0 ? kCoefVFd : kCoefEEd;
+  } else {
+    c = kind == 0 ? kCoefVF : kCoefEE;
+  }
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) eps[ax] = c * (g[ax] * g[ax] * g[ax]);
+  return kHit;
+}
+
+__device__ __forceinline__ bool params_valid(int kind, double delta, long long mc, double sep,
+                                             double t_max) {
+  return (kind == 0 || kind == 1) && delta > 0.0 && isfinite(delta) && mc >= 1 && sep >= 0.0 &&
+         isfinite(sep) && t_max > 0.0 && t_max <= 1.0;
+}
+
+// Split decision for a non-disjoint box (_kernel.py:215-241): returns the
+// final accept flag; on refine, sdim/mid/push_hi describe the children
+// (_kernel.py:259-310: VF clips only the upper child of a u or v split).
+__device__ __forceinline__ bool split_decision(const Box& b, int cls, double wb,
+                                               const double* kap, double delta, int kind,
+                                               int& sdim, double& mid, bool& push_hi) {
+  bool accept = wb < delta || cls == kContained;
+  sdim = 0;
+  mid = 0.0;
+  push_hi = true;
+  if (!accept) {
+    const double ct = (b.t1 - b.t0) * kap[0];
+    const double cu = (b.u1 - b.u0) * kap[1];
+    const double cv = (b.v1 - b.v0) * kap[2];
+    double best = ct;
+    if (cu > best) { sdim = 1; best = cu; }
+    if (cv > best) { sdim = 2; best = cv; }
+    const double lo = sdim == 0 ? b.t0 : (sdim == 1 ? b.u0 : b.v0);
+    const double hi = sdim == 0 ? b.t1 : (sdim == 1 ? b.u1 : b.v1);
+    mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) accept = true;  // float resolution (_kernel.py:230-241)
+    if (kind == 0) {
+      if (sdim == 1) push_hi = mid + b.v0 <= 1.0;
+      else if (sdim == 2) push_hi = b.u0 + mid <= 1.0;
+    }
+  }
+  return accept;
+}
+
+__device__ __forceinline__ void children(const Box& b, int sdim, double mid, Box& lo, Box& hi) {
+  lo = b;
+  hi = b;
+  if (sdim == 0) { lo.t1 = mid; hi.t0 = mid; }
+  else if (sdim == 1) { lo.u1 = mid; hi.u0 = mid; }
+  else { lo.v1 = mid; hi.v0 = mid; }
+}
+
+// Ordering key of a box inside a level: t_lo >= 0 is never -0 (domain
+// bounds are built from 0, t_max and midpoints), so its IEEE bit pattern
+// orders like the value.
+__device__ __forceinline__ unsigned long long tkey(double t) {
+  return (unsigned long long)__double_as_longlong(t);
+}
+
+}  // namespace tccd

@@ -1,0 +1,279 @@
+"""Batched conservative CCD on the GPU, behind the reference's solve API.
+
+``solve(q, config)`` has the signature, result type and exceptions of
+``ccdkit.solver.solve`` (pkg/src/ccdkit/solver.py:50-107).
+``solve_batch`` is its batched form: the same semantics per query, with
+every per-query parameter either broadcast or given as a tensor, computed by
+libtccd.so on the current CUDA stream.  There is no CPU path: without a GPU
+and the built library, both raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import CCDResult, DomainBox, Query, QueryKind, SolverConfig
+from .inclusion import FilterEps
+
+OUTPUT_FIELDS = ("status", "toi", "tol", "codom", "checks", "early", "witness", "level")
+
+_workspaces: dict = {}
+
+
+def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
+    key = (device.type, device.index)
+    ws = _workspaces.get(key)
+    if ws is None or ws.numel() < nbytes:
+        _workspaces.pop(key, None)
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _workspaces[key] = ws
+    return ws
+
+
+def release_workspaces() -> None:
+    _workspaces.clear()
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous shard [lo, hi) of n queries for rank of world."""
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def default_heavy_blocks(device: torch.device) -> int:
+    return torch.cuda.get_device_properties(device).multi_processor_count
+
+
+def workspace_bytes(n: int, max_checks_max: int, heavy_blocks: int) -> int:
+    return int(_lib.lib().tccd_workspace_bytes(int(n), int(max_checks_max), int(heavy_blocks)))
+
+
+def _param(x, n, dtype, device, name):
+    """-> (tensor or None, scalar).  Scalars broadcast; tensors are per query."""
+    if isinstance(x, (int, float, np.integer, np.floating)):
+        return None, x
+    t = torch.as_tensor(x)
+    if t.ndim == 0:
+        return None, t.item()
+    if t.shape != (n,):
+        raise ValueError(f"{name} must be a scalar or have shape ({n},), got {tuple(t.shape)}")
+    return t.to(device=device, dtype=dtype, non_blocking=True).contiguous(), 0
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
+                max_checks=None, separation=None, t_max=None, eps=None,
+                outputs=OUTPUT_FIELDS, device=None, heavy_only: bool = False,
+                heavy_blocks: int | None = None, raise_on_error: bool = True,
+                stats: bool = False) -> dict:
+    """Solve a batch of CCD queries on one GPU.
+
+    points: [n, 8, 3] float64 (torch tensor or numpy), start block then end
+    block per query (Query.all_coordinates()).  kind: [n] (0 VF, 1 EE) or a
+    scalar.  delta / max_checks / separation / t_max: scalars or [n]
+    tensors; unset ones come from ``config`` (default SolverConfig()).
+    eps: None ("auto" filters, computed per query on the device), or [3] /
+    [n, 3] caller filters; ``config.filters`` given as a FilterEps applies to
+    every query and must match its kind and separation (solver.py:30-47).
+
+    Host (CPU / numpy) inputs are copied to the device and the results come
+    back on the host; device inputs stay on their device.  Returns a dict of
+    tensors keyed by ``outputs`` (subset of OUTPUT_FIELDS; status and toi are
+    always present).
+    """
+    config = config or SolverConfig()
+    host_in = not (isinstance(points, torch.Tensor) and points.is_cuda)
+    dev = torch.device(device) if device is not None else (
+        points.device if not host_in else torch.device("cuda", torch.cuda.current_device()))
+    if dev.type != "cuda":
+        raise RuntimeError("solve_batch needs a CUDA device (there is no CPU fallback)")
+    lib = _lib.lib()
+    pts = torch.as_tensor(points)
+    if pts.dtype != torch.float64:
+        raise TypeError("points must be float64")
+    pts = pts.reshape(-1, 8, 3)
+    n = int(pts.shape[0])
+    if host_in:
+        pts = pts.contiguous().pin_memory() if pts.device.type == "cpu" else pts
+    pts = pts.to(dev, non_blocking=True).contiguous()
+
+    if isinstance(kind, (int, np.integer, QueryKind)):
+        kind_t, kind_all = None, int(kind)
+    else:
+        kind_t, kind_all = _param(kind, n, torch.uint8, dev, "kind")
+        kind_all = int(kind_all)
+    delta_t, delta_all = _param(config.delta if delta is None else delta, n, torch.float64, dev, "delta")
+    mc_src = config.max_checks if max_checks is None else max_checks
+    mc_t, mc_all = _param(mc_src, n, torch.int64, dev, "max_checks")
+    sep_src = config.separation if separation is None else separation
+    sep_t, sep_all = _param(sep_src, n, torch.float64, dev, "separation")
+    tm_t, tm_all = _param(config.t_max if t_max is None else t_max, n, torch.float64, dev, "t_max")
+    if mc_t is not None:
+        mc_max = int(torch.as_tensor(mc_src).max().item()) if n else 1
+    else:
+        mc_max = int(mc_all)
+
+    if eps is None and config.filters != "auto":
+        f = config.filters
+        if not isinstance(f, FilterEps):
+            raise TypeError("config.filters must be 'auto' or a FilterEps")
+        kinds = torch.as_tensor(kind).reshape(-1) if kind_t is not None else torch.tensor([kind_all])
+        if bool((kinds.to(torch.int64) != int(f.kind)).any()):
+            raise ValueError(f"filter set is for {f.kind.name}, a query has the other kind")
+        if sep_t is not None or f.separation != float(sep_all):
+            raise ValueError(f"filter set was computed for separation {f.separation}, "
+                             f"config has {sep_src}")
+        eps = f.eps
+    eps_t = None
+    if eps is not None:
+        e = torch.as_tensor(eps, dtype=torch.float64)
+        eps_t = e.reshape(1, 3).expand(n, 3) if e.numel() == 3 else e.reshape(n, 3)
+        eps_t = eps_t.to(dev).contiguous()
+
+    want = set(outputs) | {"status", "toi"}
+    out = {
+        "status": torch.empty(n, dtype=torch.uint8, device=dev),
+        "toi": torch.empty(n, dtype=torch.float64, device=dev),
+    }
+    if "tol" in want: out["tol"] = torch.empty(n, dtype=torch.float64, device=dev)
+    if "codom" in want: out["codom"] = torch.empty(n, dtype=torch.float64, device=dev)
+    if "checks" in want: out["checks"] = torch.empty(n, dtype=torch.int64, device=dev)
+    if "early" in want: out["early"] = torch.empty(n, dtype=torch.uint8, device=dev)
+    if "witness" in want: out["witness"] = torch.empty((n, 6), dtype=torch.float64, device=dev)
+    if "level" in want: out["level"] = torch.empty(n, dtype=torch.int32, device=dev)
+    st = torch.zeros(4, dtype=torch.int64, device=dev) if stats else None
+
+    hb = heavy_blocks or default_heavy_blocks(dev)
+    with torch.cuda.device(dev):
+        nbytes = workspace_bytes(n, mc_max, hb)
+        ws = _workspace(dev, nbytes)
+        b = _lib.TccdBatch()
+        b.struct_size = ctypes.sizeof(_lib.TccdBatch)
+        b.flags = _lib.FLAG_HEAVY_ONLY if heavy_only else 0
+        b.n = n
+        b.points = _ptr(pts)
+        b.kind = _ptr(kind_t)
+        b.kind_all = kind_all
+        b.delta = _ptr(delta_t)
+        b.delta_all = float(delta_all)
+        b.max_checks = _ptr(mc_t)
+        b.max_checks_all = int(mc_all)
+        b.max_checks_max = mc_max
+        b.separation = _ptr(sep_t)
+        b.separation_all = float(sep_all)
+        b.t_max = _ptr(tm_t)
+        b.t_max_all = float(tm_all)
+        b.eps = _ptr(eps_t)
+        for k in OUTPUT_FIELDS:
+            setattr(b, k, _ptr(out.get(k)))
+        b.workspace = _ptr(ws)
+        b.workspace_bytes = ws.numel()
+        b.heavy_blocks = hb
+        b.device_sms = default_heavy_blocks(dev)
+        b.stats = _ptr(st)
+        stream = torch.cuda.current_stream(dev)
+        rc = lib.tccd_solve_batch(ctypes.byref(b), ctypes.c_void_p(stream.cuda_stream))
+        _raise_abi(rc, delta_all, mc_all, tm_all, sep_all, kind_all)
+    if host_in:
+        out = {k: v.to("cpu", non_blocking=True) for k, v in out.items()}
+        torch.cuda.current_stream(dev).synchronize()
+    if st is not None:
+        out["stats"] = st
+    if raise_on_error and n:
+        _raise_status(out["status"])
+    return out
+
+
+def _raise_abi(rc, delta, mc, tm, sep, kind):
+    if rc == 0:
+        return
+    if rc == 3:
+        raise ValueError("delta must be positive and finite")
+    if rc == 4:
+        raise ValueError("max_checks must be >= 1")
+    if rc == 5:
+        raise ValueError("t_max must lie in (0, 1]")
+    if rc == 6:
+        raise ValueError("separation must be >= 0 and finite")
+    if rc == 7:
+        raise ValueError(f"kind must be 0 or 1, got {kind}")
+    _lib.check(rc, "tccd_solve_batch")
+
+
+def _raise_status(status: torch.Tensor) -> None:
+    bad = status >= 2
+    if not bool(bad.any()):
+        return
+    i = int(torch.nonzero(bad)[0].item())
+    code = int(status[i].item())
+    msg = {
+        _lib.STATUS_ERR_SEPARATION: "separation must be smaller than every gamma (compute_filters)",
+        _lib.STATUS_ERR_NONFINITE: "coordinates must be finite",
+        _lib.STATUS_ERR_PARAM: "per-query delta/max_checks/separation/t_max/kind out of range",
+    }.get(code, f"status {code}")
+    raise ValueError(f"query {i}: {msg}")
+
+
+def solve(q: Query, config: SolverConfig | None = None) -> CCDResult:
+    """Conservative time of impact for one query (ccdkit.solver.solve)."""
+    config = config or SolverConfig()
+    eps = None
+    if config.filters != "auto":
+        f = config.filters
+        if not isinstance(f, FilterEps):
+            raise TypeError("config.filters must be 'auto' or a FilterEps")
+        if f.kind != q.kind:
+            raise ValueError(f"filter set is for {f.kind.name}, query is {q.kind.name}")
+        if f.separation != config.separation:
+            raise ValueError(f"filter set was computed for separation {f.separation}, "
+                             f"config has {config.separation}")
+        eps = f.eps
+    pts = torch.from_numpy(q.all_coordinates()).reshape(1, 8, 3)
+    r = solve_batch(pts, int(q.kind), SolverConfig(config.delta, config.max_checks,
+                                                   config.separation, config.t_max),
+                    eps=eps)
+    status = int(r["status"][0])
+    checks = int(r["checks"][0])
+    if status == _lib.STATUS_FREE:
+        return CCDResult(None, None, 0.0, 0.0, checks, False)
+    w = r["witness"][0].tolist()
+    return CCDResult(
+        toi=float(r["toi"][0]),
+        witness=DomainBox((w[0], w[1]), (w[2], w[3]), (w[4], w[5]), int(r["level"][0])),
+        achieved_tol=float(r["tol"][0]),
+        codomain_width=float(r["codom"][0]),
+        checks=checks,
+        early_terminated=bool(r["early"][0]),
+    )
+
+
+def solve_kernel(s, e, kind, t_max, delta, max_checks, sep, ex, ey, ez):
+    """Same arguments and 13-tuple as ccdkit._kernel.solve_kernel, on the GPU
+    (through the C-ABI's tccd_solve_kernel)."""
+    s = np.ascontiguousarray(s, dtype=np.float64).reshape(4, 3)
+    e = np.ascontiguousarray(e, dtype=np.float64).reshape(4, 3)
+    out = np.zeros(13)
+    rc = _lib.lib().tccd_solve_kernel(
+        s.ctypes.data_as(ctypes.c_void_p), e.ctypes.data_as(ctypes.c_void_p), int(kind),
+        float(t_max), float(delta), int(max_checks), float(sep), float(ex), float(ey),
+        float(ez), out.ctypes.data_as(ctypes.c_void_p))
+    _lib.check(rc, "tccd_solve_kernel")
+    return (int(out[0]), float(out[1]), float(out[2]), float(out[3]), int(out[4]),
+            int(out[5]), *(float(x) for x in out[6:12]), int(out[12]))
+
+
+def warm_up(device=None) -> None:
+    """Load the library and touch both engines once (solver.py:175-188)."""
+    vf = Query(QueryKind.VERTEX_FACE,
+               ((0.5, 0.5, 1.0), (0.0, 0.0, 0.0), (1.0, 0.0, 0.0), (0.0, 1.0, 0.0)),
+               ((0.5, 0.5, -1.0), (0.0, 0.0, 0.0), (1.0, 0.0, 0.0), (0.0, 1.0, 0.0)))
+    pts = torch.from_numpy(vf.all_coordinates()).reshape(1, 8, 3)
+    solve_batch(pts, 0, SolverConfig(max_checks=16), device=device)
+    solve_batch(pts, 0, SolverConfig(max_checks=16), device=device, heavy_only=True)

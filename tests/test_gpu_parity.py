@@ -1,0 +1,223 @@
+"""GPU parity: libtccd (through the C-ABI) vs the reference's outputs.
+
+* every golden set (reference numba outputs, tests/golden/) -- bit-exact on
+  all 13 result fields, through both engines (pooled light engine with heavy
+  eviction, and the block-per-query engine alone);
+* larger seeded samples of the five workloads vs the oracle (which is itself
+  pinned to the reference by tests/test_oracle_golden.py);
+* the reference's own hot-path test assertions (pkg/tests/test_solver.py)
+  re-run on the GPU through the reference-shaped API;
+* size-independent properties at full BASELINE sizes.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import GOLDEN_SETS, assert_same_results, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu(g, cuda, heavy_only=False, **kw):
+    from paper_2009_13349_b200 import solve_batch
+    r = solve_batch(torch.from_numpy(np.ascontiguousarray(g["points"])),
+                    torch.from_numpy(np.ascontiguousarray(g["kind"])),
+                    delta=torch.from_numpy(np.ascontiguousarray(g["delta"])),
+                    max_checks=torch.from_numpy(np.ascontiguousarray(g["max_checks"])),
+                    separation=torch.from_numpy(np.ascontiguousarray(g["separation"])),
+                    t_max=torch.from_numpy(np.ascontiguousarray(g["t_max"])),
+                    device=cuda, heavy_only=heavy_only, raise_on_error=False, **kw)
+    return {k: v.numpy() for k, v in r.items() if k != "stats"}
+
+
+@pytest.mark.parametrize("name", GOLDEN_SETS)
+def test_golden_bit_exact(cuda, name):
+    g = load_golden(name)
+    assert_same_results(_gpu(g, cuda), g, name)
+
+
+@pytest.mark.parametrize("name", GOLDEN_SETS)
+def test_golden_bit_exact_block_engine(cuda, name):
+    g = load_golden(name)
+    assert_same_results(_gpu(g, cuda, heavy_only=True, heavy_blocks=64), g, name + "/heavy")
+
+
+def _vs_oracle(w, cuda, sep=None, t_max=None, heavy_only=False):
+    from paper_2009_13349_b200 import solve_batch
+    sep = w.separation if sep is None else sep
+    t_max = w.t_max if t_max is None else t_max
+    ref = oracle.solve_batch(w.points, w.kind, w.delta, w.max_checks, sep, t_max)
+    got = solve_batch(torch.from_numpy(w.points), torch.from_numpy(w.kind),
+                      delta=w.delta if np.isscalar(w.delta) else torch.from_numpy(w.delta),
+                      max_checks=w.max_checks if np.isscalar(w.max_checks)
+                      else torch.from_numpy(w.max_checks),
+                      separation=sep, t_max=t_max, device=cuda, heavy_only=heavy_only,
+                      raise_on_error=False)
+    assert_same_results({k: v.numpy() for k, v in got.items()}, ref,
+                        f"{w.meta['name']}[{w.meta['start']}:+{w.n}]")
+    return ref
+
+
+@pytest.mark.parametrize("config,start,count,kw", [
+    (0, 0, 10_000, {}),
+    (0, 0, 10_000, dict(t_max=0.3)),
+    (0, 0, 10_000, dict(t_max=0.7)),
+    (1, 10_000, 20_000, {}),
+    (2, 5_000, 3_000, {}),
+    (3, 100_000, 50_000, {}),
+    (4, 20_000, 30_000, dict(sep=1e-8)),
+    (4, 60_000, 300, dict(sep=1e-5)),
+    (4, 61_000, 40, dict(sep=1e-3)),
+])
+def test_workload_samples_vs_oracle(cuda, config, start, count, kw):
+    from paper_2009_13349_b200 import workloads as W
+    w = W.generate(config, start, count, separation=kw.get("sep"))
+    _vs_oracle(w, cuda, sep=kw.get("sep"), t_max=kw.get("t_max"))
+
+
+def test_heavy_tail_sample_block_engine(cuda):
+    from paper_2009_13349_b200 import workloads as W
+    w = W.generate(2, 0, 400)
+    _vs_oracle(w, cuda, heavy_only=True)
+
+
+# --- the reference's own solver assertions (pkg/tests/test_solver.py) -------
+
+TRI = ((0.0, 0.0, 0.0), (1.0, 0.0, 0.0), (0.0, 1.0, 0.0))
+
+
+def _q(kind, p0, p1):
+    from paper_2009_13349_b200 import Query, QueryKind
+    return Query(QueryKind(kind), p0, p1)
+
+
+def test_reference_solver_assertions(cuda):
+    from paper_2009_13349_b200 import (CCDResult, QueryKind, SolverConfig, compute_filters,
+                                       compute_gamma, solve)
+    vf_vertical = _q(0, ((0.3, 0.3, 1.0),) + TRI, ((0.3, 0.3, -1.0),) + TRI)
+    vf_offset = _q(0, ((0.0, 0.0, 10.0),) + TRI, ((0.0, 0.0, 10.0),) + TRI)
+    ee = _q(1, ((0.0, 0.0, 1.0), (1.0, 1.0, 1.0), (0.0, 1.0, 0.0), (1.0, 0.0, 0.0)),
+            ((0.0, 0.0, -1.0), (1.0, 1.0, -1.0), (0.0, 1.0, 0.0), (1.0, 0.0, 0.0)))
+    res = solve(vf_vertical)
+    assert res.colliding and res.toi <= 0.5 and 0.5 - res.toi < 2e-6
+    assert res.achieved_tol <= 1e-6 and not res.early_terminated
+    assert solve(vf_offset) == CCDResult(None, None, 0.0, 0.0, 1, False)
+    r = solve(ee)
+    assert r.colliding and r.toi <= 0.5 and 0.5 - r.toi < 2e-6
+    hour = _q(0, ((0.1, 0.1, 0.1), (0.0, 0.0, 1.0), (1.0, 0.0, 1.0), (0.0, 1.0, 1.0)),
+              ((0.1, 0.1, 0.1), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), (1.0, 0.0, 0.0)))
+    hr = solve(hour)
+    from fractions import Fraction
+    HT = Fraction(32425917317067571, 36028797018963968)
+    assert hr.colliding and Fraction(hr.toi) <= HT and HT - Fraction(hr.toi) < Fraction(1, 10**4)
+    touch = _q(0, ((0.3, 0.3, 0.0),) + TRI, ((0.3, 0.3, -1.0),) + TRI)
+    assert solve(touch).toi == 0.0
+    assert solve(vf_vertical) == solve(vf_vertical)
+    near = lambda g: _q(0, ((0.3, 0.3, 1.0),) + TRI, ((0.3, 0.3, g),) + TRI)
+    assert solve(near(1e-8)).toi is None and solve(near(1e-12)).toi is None
+    assert solve(near(1e-16)).colliding
+    assert solve(vf_vertical, SolverConfig(t_max=0.3)).toi is None
+    b = solve(vf_vertical, SolverConfig(max_checks=5))
+    assert b.early_terminated and b.checks <= 5 and b.toi is not None and b.toi <= 0.5
+    d = solve(vf_vertical, SolverConfig(separation=0.1))
+    assert d.colliding and d.toi <= 0.45 and 0.45 - d.toi <= d.achieved_tol
+    gamma = compute_gamma(vf_vertical.all_coordinates())
+    manual = SolverConfig(filters=compute_filters(QueryKind.VERTEX_FACE, gamma))
+    assert solve(vf_vertical, manual) == solve(vf_vertical)
+    with pytest.raises(ValueError):
+        solve(vf_vertical, SolverConfig(filters=compute_filters(QueryKind.EDGE_EDGE, (1, 1, 1))))
+    with pytest.raises(ValueError):
+        solve(vf_vertical, SolverConfig(
+            filters=compute_filters(QueryKind.VERTEX_FACE, (1, 1, 1), separation=0.5)))
+    with pytest.raises(TypeError):
+        solve(vf_vertical, SolverConfig(filters=(1e-15, 1e-15, 1e-15)))
+    with pytest.raises(ValueError):
+        solve(vf_vertical, SolverConfig(separation=2.0))  # d >= gamma
+
+
+def test_solve_kernel_drop_in(cuda):
+    from paper_2009_13349_b200 import solve_kernel
+    g = load_golden("kat")
+    for i in range(len(g["kind"])):
+        if g["status"][i] >= 2:
+            continue
+        pts = g["points"][i]
+        from test_oracle_golden import oracle_eps
+        eps = oracle_eps(pts, int(g["kind"][i]), float(g["separation"][i]))
+        args = (pts[:4], pts[4:], int(g["kind"][i]), g["t_max"][i], g["delta"][i],
+                int(g["max_checks"][i]), g["separation"][i], *eps)
+        assert solve_kernel(*args) == oracle.solve_kernel(*args)
+
+
+def test_batch_edge_cases(cuda):
+    from paper_2009_13349_b200 import solve_batch
+    empty = solve_batch(torch.zeros((0, 8, 3), dtype=torch.float64), 0, device=cuda)
+    assert empty["status"].numel() == 0
+    g = load_golden("c0")
+    pts = torch.from_numpy(g["points"][:64].copy())
+    bad = pts.clone()
+    bad[3, 2, 1] = float("nan")
+    r = solve_batch(bad, 0, device=cuda, raise_on_error=False)
+    assert int(r["status"][3]) == 3 and math.isinf(float(r["toi"][3]))
+    with pytest.raises(ValueError):
+        solve_batch(bad, 0, device=cuda)
+    with pytest.raises(ValueError):
+        solve_batch(pts, 0, delta=0.0, device=cuda)
+    with pytest.raises(ValueError):
+        solve_batch(pts, 0, t_max=1.5, device=cuda)
+    # per-query invalid parameter -> status 4 on that query only
+    mc = torch.full((64,), 1000, dtype=torch.int64)
+    mc[5] = 0
+    r = solve_batch(pts, 0, max_checks=mc, device=cuda, raise_on_error=False)
+    assert int(r["status"][5]) == 4 and int((r["status"] >= 2).sum()) == 1
+    # device-resident inputs give identical results to host inputs
+    rd = solve_batch(pts.to(cuda), torch.zeros(64, dtype=torch.uint8, device=cuda), device=cuda)
+    rh = solve_batch(pts, 0, device=cuda)
+    for k in rh:
+        assert torch.equal(rd[k].cpu(), rh[k])
+
+
+def test_shard_invariance(cuda):
+    """Results do not depend on how a batch is split (multi-GPU sharding)."""
+    from paper_2009_13349_b200 import shard_bounds, solve_batch
+    from paper_2009_13349_b200 import workloads as W
+    w = W.generate(1, 0, 8192)
+    full = solve_batch(torch.from_numpy(w.points), torch.from_numpy(w.kind), device=cuda)
+    for world in (2, 3, 8):
+        parts = []
+        for r in range(world):
+            lo, hi = shard_bounds(w.n, world, r)
+            parts.append(solve_batch(torch.from_numpy(w.points[lo:hi]),
+                                     torch.from_numpy(w.kind[lo:hi]), device=cuda))
+        for k in full:
+            assert torch.equal(torch.cat([p[k] for p in parts]), full[k])
+
+
+def test_full_config1_properties(cuda):
+    """Full-size config 1 (10^6 queries): every planted root is reported with a
+    conservative toi (toi <= t*, exact rational comparison is exact here
+    because both are binary64), results are deterministic run to run, and a
+    seeded stratified subsample matches the oracle bit for bit."""
+    from paper_2009_13349_b200 import solve_batch
+    from paper_2009_13349_b200 import workloads as W
+    w = W.generate(1)
+    pts = torch.from_numpy(w.points).to(cuda)
+    kind = torch.from_numpy(w.kind).to(cuda)
+    r1 = solve_batch(pts, kind, device=cuda)
+    r2 = solve_batch(pts, kind, device=cuda)
+    for k in r1:
+        assert torch.equal(r1[k], r2[k])
+    planted = ~np.isnan(w.planted_t)
+    st = r1["status"].cpu().numpy()
+    toi = r1["toi"].cpu().numpy()
+    assert (st[planted] == 1).all(), "a planted root was missed (false negative)"
+    assert (toi[planted] <= w.planted_t[planted]).all(), "toi after the planted root"
+    idx = np.random.default_rng(7).choice(w.n, 4000, replace=False)
+    idx.sort()
+    sub = {k: v.cpu().numpy()[idx] for k, v in r1.items()}
+    ref = oracle.solve_batch(w.points[idx], w.kind[idx])
+    assert_same_results(sub, ref, "config1 subsample")
