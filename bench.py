@@ -231,6 +231,8 @@ def main():
     checks = full["checks"].cpu().numpy()
     hits = int((full["status"] == 1).sum().item())
     evicted = int(full["stats"][0].item())
+    pool_rounds = int(full["stats"][1].item())
+    deferrals = int(full["stats"][2].item())
     flops = algorithmic_flops(w.kind, checks)
     for _ in range(args.warmup):
         step()
@@ -302,7 +304,8 @@ def main():
         "clocks": clk,
         "gpu_launches": 2 * args.steps * 2,
         "workload_stats": {"hits": hits, "hit_rate": hits / Q, "mean_checks": float(checks.mean()),
-                           "max_checks": int(checks.max()), "evicted_to_block_engine": evicted},
+                           "max_checks": int(checks.max()), "evicted_to_block_engine": evicted,
+                           "pool_rounds": pool_rounds, "pool_deferrals": deferrals},
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -186,11 +186,17 @@ static void stable_order(const double *keys, int64_t n, int64_t *ord, int64_t *t
   }
 }
 
+/* diagnostics: boxes visited per level, bucketed by floor(log2(level width))
+ * (includes boxes past an early return in their level) */
+int64_t tccd_oracle_level_hist[64];
+
 typedef struct {
   box_t *cur, *nxt;
   double *keys;
   int64_t *ord, *tmp;
   int64_t cap;
+  int64_t max_frontier; /* diagnostics of the last solve: widest level */
+  int64_t levels;       /* and number of levels visited */
 } arena_t;
 
 static int arena_reserve(arena_t *a, int64_t need) {
@@ -250,7 +256,14 @@ static int solve_one(const double *s, const double *e, int kind, double t_max,
   int f_level = 0, d_level = 0;
   double f_codom = 0.0, d_codom = 0.0;
 
+  ar->max_frontier = 0;
+  ar->levels = 0;
+  extern int64_t tccd_oracle_level_hist[64];
   while (ncur > 0) {
+    if (ncur > ar->max_frontier) ar->max_frontier = ncur;
+    ar->levels++;
+    __atomic_fetch_add(&tccd_oracle_level_hist[63 - __builtin_clzll((unsigned long long)ncur)],
+                       ncur, __ATOMIC_RELAXED);
     for (int64_t i = 0; i < ncur; ++i) ar->keys[i] = cur[i].t0;
     stable_order(ar->keys, ncur, ar->ord, ar->tmp);
     for (int64_t oi = 0; oi < ncur; ++oi) {
@@ -383,6 +396,7 @@ typedef struct {
   uint8_t *early;
   double *witness;
   int32_t *level;
+  int64_t *frontier; /* optional diagnostics [n][2]: widest level, levels */
   /* work distribution */
   int64_t next;
   int64_t chunk;
@@ -430,6 +444,10 @@ static void solve_index(batch_t *B, int64_t q, arena_t *ar) {
   if (B->early) B->early[q] = (uint8_t)r.early;
   if (B->witness) memcpy(B->witness + 6 * q, r.w, 6 * sizeof(double));
   if (B->level) B->level[q] = r.level;
+  if (B->frontier) {
+    B->frontier[2 * q] = st == ST_HIT ? ar->max_frontier : 0;
+    B->frontier[2 * q + 1] = st == ST_HIT ? ar->levels : 0;
+  }
 }
 
 static void *worker(void *arg) {
@@ -452,7 +470,7 @@ int tccd_oracle_solve_batch(int64_t n, const double *points, const uint8_t *kind
                             double t_max_all, const double *eps, uint8_t *status,
                             double *toi, double *tol, double *codom, int64_t *checks,
                             uint8_t *early, double *witness, int32_t *level,
-                            int threads) {
+                            int64_t *frontier, int threads) {
   batch_t B;
   memset(&B, 0, sizeof(B));
   B.n = n; B.points = points; B.kind = kind; B.kind_all = kind_all;
@@ -460,7 +478,7 @@ int tccd_oracle_solve_batch(int64_t n, const double *points, const uint8_t *kind
   B.max_checks_all = max_checks_all; B.sep = sep; B.sep_all = sep_all;
   B.t_max = t_max; B.t_max_all = t_max_all; B.eps = eps; B.status = status;
   B.toi = toi; B.tol = tol; B.codom = codom; B.checks = checks; B.early = early;
-  B.witness = witness; B.level = level;
+  B.witness = witness; B.level = level; B.frontier = frontier;
   B.chunk = 16;
   if (threads < 1) threads = 1;
   if (threads == 1) {

@@ -4,16 +4,15 @@
 // reference state machine (ccdkit._kernel.solve_kernel, pkg/src/ccdkit/
 // _kernel.py:136-324) exactly, per query:
 //
-//  * light engine (light_kernel): a persistent CTA keeps a pool of up to
-//    kLQ queries resident in shared memory, together with the current BFS
-//    level of every one of them as one flat box list.  Each round, every
-//    thread classifies one box of the flat list (lane-per-box, all queries
-//    mixed, so trivially separated queries do not idle a warp), then one
-//    thread per query replays the reference's in-level event sequence over
-//    the precomputed classes (budget cut, first/drop records, accept,
-//    children in push order, stable t_lo order of the next level) and
-//    retires, continues or evicts the query; free slots are refilled from a
-//    global work counter (dynamic load balance across CTAs).
+//  * pool engine (pool_kernel, tccd_pool.cuh): a persistent CTA keeps up to
+//    kPQ queries resident and advances all of them one BFS level per
+//    round.  Every thread classifies boxes of the flat list of all resident
+//    levels (lane per box, queries mixed, so trivially separated queries do
+//    not idle a warp); the in-level event sequence of each query (budget
+//    cut, first/drop records, accept, children in push order, stable t_lo
+//    order of the next level) is recovered with segmented block-wide mins,
+//    scans and merge-by-rank; finished slots are refilled from a global
+//    work counter (dynamic load balance across CTAs).
 //  * heavy engine (heavy_kernel): one CTA per query with the level in a
 //    global-memory arena sized for the worst case (2 * m_I boxes), used for
 //    queries whose frontier outgrows the light pool.  The level is
@@ -39,22 +38,15 @@ namespace tccd {
 
 // ---------------------------------------------------------------------------
 // launch geometry / pool sizes
-constexpr int kLB = 256;    // light engine threads per CTA
-constexpr int kLQ = 128;    // query slots per light CTA
-constexpr int kLCap = 512;  // boxes per light level buffer
-constexpr int kQCap = 64;   // largest per-query level the light engine keeps
 constexpr int kHB = 256;    // heavy engine threads per CTA
-constexpr uint8_t kNoSlot = 0xFF;
-
-static_assert(kLQ <= kLB, "one resolver thread per slot");
-static_assert(kLQ < 255, "slot ids are u8");
 
 struct Counters {
-  unsigned long long light_next;   // next query index to admit
+  unsigned long long light_next;   // next query index the pool admits
   unsigned long long heavy_count;  // entries in the heavy queue
   unsigned long long heavy_next;   // next heavy queue entry to solve
-  unsigned long long rounds;       // light rounds (diagnostics)
-  unsigned long long pad[4];
+  unsigned long long rounds;       // pool rounds (diagnostics)
+  unsigned long long deferred;     // pool level deferrals (diagnostics)
+  unsigned long long pad[3];
 };
 
 struct Args {
@@ -83,6 +75,8 @@ struct Args {
   long long* stats;
   Counters* ctr;
   long long* heavy_queue;
+  unsigned char* pool_arenas;
+  size_t pool_arena_bytes;
   unsigned char* arenas;
   size_t arena_bytes;
   long long cap;  // boxes per heavy arena buffer
@@ -137,7 +131,7 @@ __device__ __forceinline__ uint8_t prologue(const Args& a, long long q, PtrT P, 
 }
 
 // ---------------------------------------------------------------------------
-// block scan (kHB or kLB threads)
+// block scan (NT threads)
 template <int NT>
 __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
                                                               unsigned long long* sw,
@@ -480,272 +474,17 @@ __global__ void __launch_bounds__(kHB) heavy_kernel(Args a) {
   }
 }
 
-// ===========================================================================
-// light engine: pooled queries, lane-per-box classification
-// ===========================================================================
-struct LightShared {
-  double P[kLQ][24];
-  QueryParams qp[kLQ];
-  long long checks[kLQ];
-  long long qidx[kLQ];  // -1: free slot
-  Box fbox[kLQ], dbox[kLQ];
-  double fcodom[kLQ], dcodom[kLQ];
-  int flevel[kLQ], dlevel[kLQ];
-  int level[kLQ];
-  short seg_off[kLQ], seg_n[kLQ];
-  uint8_t have_first[kLQ], have_drop[kLQ];
-  Box buf[2][kLCap];
-  uint8_t slot_of[2][kLCap];
-  uint8_t flag[kLCap];
-  double wb[kLCap];
-  int n_cur, n_next, admit_k, exhausted;
-  long long admit_base;
-  unsigned int free_mask[kLQ / 32];
-};
+}  // namespace tccd
 
-__device__ __forceinline__ void light_finish(const Args& a, LightShared& S, int s, bool early,
-                                             long long checks) {
-  const long long q = S.qidx[s];
-  if (S.have_drop[s] && (!S.have_first[s] || S.dbox[s].t0 < S.fbox[s].t0))
-    write_result(a, q, kHit, S.dbox[s], S.dcodom[s], checks, early, S.dlevel[s]);
-  else
-    write_result(a, q, kHit, S.fbox[s], S.fcodom[s], checks, early, S.flevel[s]);
-  S.qidx[s] = -1;
-}
+#include "tccd_pool.cuh"
 
-__device__ __forceinline__ void light_free(const Args& a, LightShared& S, int s, long long checks) {
-  const Box z = {0, 0, 0, 0, 0, 0};
-  write_result(a, S.qidx[s], kFree, z, 0.0, checks, 0, 0);
-  S.qidx[s] = -1;
-}
-
-// Replay the reference's in-level loop (_kernel.py:176-312) for slot s over
-// its level (already in sorted order) using the precomputed box classes.
-// Returns the number of children to push (0 if the query finished).
-__device__ int light_resolve(const Args& a, LightShared& S, int s, int cur) {
-  const int off = S.seg_off[s], n = S.seg_n[s];
-  long long C = S.checks[s];
-  const long long mc = S.qp[s].max_checks;
-  bool seen = false;
-  int nch = 0;
-  for (int k = 0; k < n; ++k) {
-    const int i = off + k;
-    const uint8_t f = S.flag[i];
-    C += 1;
-    if ((f & 3) == kDisjoint) {
-      if (C >= mc && (S.have_drop[s] || k + 1 < n || nch > 0)) {
-        light_finish(a, S, s, true, C);
-        return 0;
-      }
-      continue;
-    }
-    const Box b = S.buf[cur][i];
-    if (!seen) {
-      S.have_first[s] = 1;
-      S.fbox[s] = b;
-      S.fcodom[s] = S.wb[i];
-      S.flevel[s] = S.level[s];
-    }
-    if (C >= mc) {
-      light_finish(a, S, s, true, C);
-      return 0;
-    }
-    if (f & 4) {
-      if (!seen) {
-        if (S.have_drop[s] && S.dbox[s].t0 < b.t0)
-          write_result(a, S.qidx[s], kHit, S.dbox[s], S.dcodom[s], C, 0, S.dlevel[s]);
-        else
-          write_result(a, S.qidx[s], kHit, b, S.wb[i], C, 0, S.level[s]);
-        S.qidx[s] = -1;
-        return 0;
-      }
-      if (!S.have_drop[s] || b.t0 < S.dbox[s].t0) {
-        S.dbox[s] = b;
-        S.dcodom[s] = S.wb[i];
-        S.dlevel[s] = S.level[s];
-      }
-      S.have_drop[s] = 1;
-    } else {
-      nch += (f & 32) ? 2 : 1;
-    }
-    seen = true;
-  }
-  S.checks[s] = C;
-  if (nch == 0) {
-    // queue exhausted (_kernel.py:321-324)
-    if (S.have_drop[s]) {
-      write_result(a, S.qidx[s], kHit, S.dbox[s], S.dcodom[s], C, 0, S.dlevel[s]);
-      S.qidx[s] = -1;
-    } else {
-      light_free(a, S, s, C);
-    }
-  }
-  return nch;
-}
-
-// Write slot s's children (push order) at dst[base..base+nch) and stable
-// insertion-sort them by t_lo (_kernel.py:174-175 on the next level).
-__device__ void light_generate(LightShared& S, int s, int cur, int base) {
-  const int off = S.seg_off[s], n = S.seg_n[s];
-  const int nxt = cur ^ 1;
-  Box* dst = S.buf[nxt];
-  int w = base;
-  for (int k = 0; k < n; ++k) {
-    const int i = off + k;
-    const uint8_t f = S.flag[i];
-    if ((f & 3) == kDisjoint || (f & 4)) continue;
-    const int sdim = (f >> 3) & 3;
-    const Box b = S.buf[cur][i];
-    const double lo = sdim == 0 ? b.t0 : (sdim == 1 ? b.u0 : b.v0);
-    const double hi = sdim == 0 ? b.t1 : (sdim == 1 ? b.u1 : b.v1);
-    Box c0, c1;
-    children(b, sdim, 0.5 * (lo + hi), c0, c1);
-    dst[w++] = c0;
-    if (f & 32) dst[w++] = c1;
-  }
-  // stable insertion sort on t_lo (strict > keeps equal keys in push order)
-  for (int x = base + 1; x < w; ++x) {
-    const Box v = dst[x];
-    int y = x - 1;
-    while (y >= base && dst[y].t0 > v.t0) {
-      dst[y + 1] = dst[y];
-      --y;
-    }
-    dst[y + 1] = v;
-  }
-  for (int x = base; x < w; ++x) S.slot_of[nxt][x] = (uint8_t)s;
-  S.seg_off[s] = (short)base;
-  S.seg_n[s] = (short)(w - base);
-  S.level[s] += 1;
-}
-
-__global__ void __launch_bounds__(kLB) light_kernel(Args a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  LightShared& S = *reinterpret_cast<LightShared*>(smem_raw);
-  const int tid = threadIdx.x;
-  if (tid < kLQ) S.qidx[tid] = -1;
-  if (tid == 0) { S.n_cur = 0; S.exhausted = 0; }
-  __syncthreads();
-  int cur = 0;
-  long long rounds = 0;
-  for (;;) {
-    // ---- admission: refill free slots with fresh queries (root boxes)
-    if (tid < 32) {
-      unsigned int cnt = 0;
-      for (int w = 0; w < kLQ / 32; ++w) {
-        const unsigned int m = __ballot_sync(0xffffffffu, S.qidx[w * 32 + tid] < 0);
-        if (tid == 0) S.free_mask[w] = m;
-        cnt += __popc(m);
-      }
-      if (tid == 0) {
-        int k = (int)cnt;
-        const int room = kLCap - S.n_cur;
-        if (k > room) k = room;
-        long long base = 0;
-        if (S.exhausted) k = 0;
-        if (k > 0) {
-          base = (long long)atomicAdd(&a.ctr->light_next, (unsigned long long)k);
-          if (base >= a.n) { k = 0; S.exhausted = 1; }
-          else if (base + k >= a.n) { k = (int)(a.n - base); S.exhausted = 1; }
-        }
-        S.admit_k = k;
-        S.admit_base = base;
-      }
-    }
-    __syncthreads();
-    const int k_adm = S.admit_k;
-    if (tid < kLQ && S.qidx[tid] < 0 && k_adm > 0) {
-      const int w = tid >> 5, lane = tid & 31;
-      int r = __popc(S.free_mask[w] & ((1u << lane) - 1u));
-      for (int ww = 0; ww < w; ++ww) r += __popc(S.free_mask[ww]);
-      if (r < k_adm) {
-        const long long q = S.admit_base + r;
-        const int pos = S.n_cur + r;
-        double* P = S.P[tid];
-        for (int i = 0; i < 24; ++i) P[i] = a.points[24 * q + i];
-        const uint8_t st = prologue(a, q, (const double*)P, S.qp[tid]);
-        if (st != kHit) {
-          const Box z = {0, 0, 0, 0, 0, 0};
-          write_result(a, q, st, z, 0.0, 0, 0, 0);
-          S.slot_of[cur][pos] = kNoSlot;
-        } else {
-          S.qidx[tid] = q;
-          S.checks[tid] = 0;
-          S.level[tid] = 0;
-          S.have_first[tid] = 0;
-          S.have_drop[tid] = 0;
-          S.seg_off[tid] = (short)pos;
-          S.seg_n[tid] = 1;
-          S.buf[cur][pos] = Box{0.0, S.qp[tid].t_max, 0.0, 1.0, 0.0, 1.0};
-          S.slot_of[cur][pos] = (uint8_t)tid;
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      S.n_cur += k_adm;
-      S.n_next = 0;
-    }
-    __syncthreads();
-    const int n_cur = S.n_cur;
-    if (n_cur == 0) break;
-    ++rounds;
-    // ---- classify every box of every resident query
-    for (int i = tid; i < n_cur; i += kLB) {
-      const int s = S.slot_of[cur][i];
-      if (s == kNoSlot) continue;
-      const Box b = S.buf[cur][i];
-      const QueryParams& qp = S.qp[s];
-      double wb;
-      const int cls = classify((const double*)S.P[s], qp.kind, b, qp.eps, qp.sep, wb);
-      uint8_t f = (uint8_t)cls;
-      if (cls != kDisjoint) {
-        int sdim; double mid; bool ph;
-        const bool acc = split_decision(b, cls, wb, qp.kap, qp.delta, qp.kind, sdim, mid, ph);
-        f = make_flag(cls, acc, sdim, ph);
-      }
-      S.flag[i] = f;
-      S.wb[i] = wb;
-    }
-    __syncthreads();
-    // ---- per-query sequential resolution + next level
-    if (tid < kLQ && S.qidx[tid] >= 0) {
-      const int s = tid;
-      const int nch = light_resolve(a, S, s, cur);
-      if (nch > 0) {
-        int base = -1;
-        if (nch <= kQCap) {
-          int old = S.n_next;
-          for (;;) {
-            if (old + nch > kLCap) break;
-            const int prev = atomicCAS(&S.n_next, old, old + nch);
-            if (prev == old) { base = old; break; }
-            old = prev;
-          }
-        }
-        if (base >= 0) {
-          light_generate(S, s, cur, base);
-        } else {
-          // frontier outgrew the pool: hand the query to the heavy engine
-          const unsigned long long h = atomicAdd(&a.ctr->heavy_count, 1ull);
-          a.heavy_queue[h] = S.qidx[s];
-          S.qidx[s] = -1;
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) S.n_cur = S.n_next;
-    cur ^= 1;
-    __syncthreads();
-  }
-  if (tid == 0) atomicAdd(&a.ctr->rounds, (unsigned long long)rounds);
-}
+namespace tccd {
 
 __global__ void stats_kernel(Args a) {
   if (threadIdx.x == 0 && a.stats) {
     a.stats[0] = a.heavy_only ? a.n : (long long)a.ctr->heavy_count;
     a.stats[1] = (long long)a.ctr->rounds;
-    a.stats[2] = 0;
+    a.stats[2] = (long long)a.ctr->deferred;
     a.stats[3] = 0;
   }
 }
@@ -771,18 +510,22 @@ long long heavy_cap(long long mcmax) { return 2 * mcmax + 2; }
 
 int default_heavy_blocks(int sms) { return sms; }
 
-size_t layout(long long n, long long mcmax, int hb, size_t* off_queue, size_t* off_arenas,
-              size_t* arena_b) {
+int pool_blocks(int sms) { return 2 * sms; }
+
+size_t layout(long long n, long long mcmax, int hb, int sms, size_t* off_queue,
+              size_t* off_pool, size_t* off_arenas, size_t* arena_b) {
   const size_t ctr = align256(sizeof(Counters));
   const size_t q = align256((size_t)(n > 0 ? n : 1) * sizeof(long long));
+  const size_t pool = pool_arena_bytes() * (size_t)pool_blocks(sms);
   const size_t ab = arena_bytes_for(heavy_cap(mcmax));
   if (off_queue) *off_queue = ctr;
-  if (off_arenas) *off_arenas = ctr + q;
+  if (off_pool) *off_pool = ctr + q;
+  if (off_arenas) *off_arenas = ctr + q + pool;
   if (arena_b) *arena_b = ab;
-  return ctr + q + ab * (size_t)hb;
+  return ctr + q + pool + ab * (size_t)hb;
 }
 
-bool light_configured = false;
+bool pool_configured = false;
 
 }  // namespace
 
@@ -810,8 +553,9 @@ const char* tccd_error_string(int code) {
 
 size_t tccd_workspace_bytes(int64_t n, int64_t max_checks_max, int32_t heavy_blocks) {
   if (n < 0 || max_checks_max < 1) return 0;
-  const int hb = heavy_blocks > 0 ? heavy_blocks : default_heavy_blocks(device_sm_count(0));
-  return layout(n, max_checks_max, hb, nullptr, nullptr, nullptr);
+  const int sms = device_sm_count(0);
+  const int hb = heavy_blocks > 0 ? heavy_blocks : default_heavy_blocks(sms);
+  return layout(n, max_checks_max, hb, sms, nullptr, nullptr, nullptr, nullptr);
 }
 
 int tccd_solve_batch(const tccd_batch* b, void* stream) {
@@ -830,8 +574,8 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
   if (mcmax > (1LL << 30)) return TCCD_E_CAPACITY;  // push indices are u32
   const int sms = device_sm_count(b->device_sms);
   const int hb = b->heavy_blocks > 0 ? b->heavy_blocks : default_heavy_blocks(sms);
-  size_t off_q, off_ar, arena_b;
-  const size_t need = layout(b->n, mcmax, hb, &off_q, &off_ar, &arena_b);
+  size_t off_q, off_pool, off_ar, arena_b;
+  const size_t need = layout(b->n, mcmax, hb, sms, &off_q, &off_pool, &off_ar, &arena_b);
   if (!b->workspace || b->workspace_bytes < need) return TCCD_E_WORKSPACE;
   if (b->n == 0) return TCCD_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -864,6 +608,8 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
   a.stats = (long long*)b->stats;
   a.ctr = (Counters*)ws;
   a.heavy_queue = (long long*)(ws + off_q);
+  a.pool_arenas = ws + off_pool;
+  a.pool_arena_bytes = pool_arena_bytes();
   a.arenas = ws + off_ar;
   a.arena_bytes = arena_b;
   a.cap = heavy_cap(mcmax);
@@ -871,22 +617,17 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
 
   if (cudaMemsetAsync(ws, 0, sizeof(Counters), st) != cudaSuccess) return TCCD_E_CUDA;
   if (!a.heavy_only) {
-    const int smem = (int)sizeof(LightShared);
-    if (!light_configured) {
-      if (cudaFuncSetAttribute(light_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+    const int smem = (int)sizeof(PoolShared);
+    if (!pool_configured) {
+      if (cudaFuncSetAttribute(pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
           cudaSuccess)
         return TCCD_E_CUDA;
-      light_configured = true;
+      pool_configured = true;
     }
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, light_kernel, kLB, smem) !=
-            cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
-    long long grid = (long long)per_sm * sms;
-    const long long need_blocks = (b->n + kLQ - 1) / kLQ;
+    long long grid = pool_blocks(sms);
+    const long long need_blocks = (b->n + kPQ - 1) / kPQ;
     if (grid > need_blocks) grid = need_blocks;
-    light_kernel<<<(unsigned)grid, kLB, smem, st>>>(a);
+    pool_kernel<<<(unsigned)grid, kPT, smem, st>>>(a);
     if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
   }
   long long hgrid = hb;
@@ -910,7 +651,7 @@ int tccd_solve_kernel(const double* s, const double* e, int kind, double t_max, 
   memcpy(hpts, s, 12 * sizeof(double));
   memcpy(hpts + 12, e, 12 * sizeof(double));
   const int hb = 1;
-  const size_t ws_bytes = tccd_workspace_bytes(1, max_checks, hb);
+  const size_t ws_bytes = tccd_workspace_bytes(1, max_checks, hb);  // pool arenas unused (heavy-only)
   // one allocation: inputs | outputs | workspace
   const size_t in_b = 256, out_b = 256;
   unsigned char* d = nullptr;

@@ -26,7 +26,7 @@ constexpr double kCoefEE = 6.217248937900877e-15;
 constexpr double kCoefVFd = 7.549516567451064e-15;
 constexpr double kCoefEEd = 7.105427357601002e-15;
 
-struct Box {
+struct alignas(16) Box {
   double t0, t1, u0, u1, v0, v1;
 };
 
