@@ -114,9 +114,11 @@ typedef struct tccd_batch {
   size_t workspace_bytes;
   int32_t heavy_blocks; /* concurrent block-per-query solvers; 0 = default   */
   int32_t device_sms;   /* SM count of the target device; 0 = query it      */
-  int64_t *stats;       /* optional device [4]: [0] queries moved to the
-                           block-per-query engine, [1] light-engine rounds,
-                           [2..3] reserved (written as 0)                  */
+  int64_t *stats;       /* optional device [8] diagnostics: [0] queries
+                           that reached the giant tier, [1] engine rounds,
+                           [2] level deferrals, [3] queries that reached the
+                           medium tier, [4..6] boxes visited per tier
+                           (light, medium, giant), [7] reserved           */
 } tccd_batch;
 
 /* Bytes of device workspace tccd_solve_batch needs for a batch of n queries

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtccd.so")
+LIB_PATH = os.environ.get("TCCD_LIB") or os.path.join(_HERE, "libtccd.so")  # override: experiments only
 
 ABI_VERSION = 1
 FLAG_HEAVY_ONLY = 1

@@ -1,0 +1,756 @@
+// Level engine: an independent group of threads (a warp, or a whole CTA)
+// keeps up to Q queries resident and advances all of them one BFS level per
+// round.  One template, three tiers (see tccd.cu): light and medium (one warp
+// per group, many independent groups per SM, warp-synchronous: the latency
+// of one group's memory phases is hidden by the others) and giant (a CTA per
+// query for levels of up to 2 * m_I boxes).  A query whose level outgrows
+// its tier is restarted in the next tier (classification is a pure function
+// of the box, so the replay is exact).
+//
+// Representation.  The current levels of all resident queries form one flat
+// list of 4-byte references, one segment per query, each segment in the
+// reference's visiting order (stable by t_lo, _kernel.py:174-175).  A
+// reference names a box of the PREVIOUS round's materialized box array:
+// "child cb of box src" (the split is recomputed from the parent, a pure
+// function of the parent box and kappa), "box src itself" (a deferred
+// level), or the query's root.  Children never travel through memory as
+// boxes: the classify phase materializes each box once, in visiting order.
+//
+// A round:
+//   P1 materialize + classify every box (lane per box, queries mixed);
+//      group-wide atomicMin per query = first non-disjoint box j
+//   P2 atomicMin per query = first accepted box after j before the budget
+//      cut (the only box that can become the "drop" record)
+//   P3 one thread per query replays the reference's in-level events from
+//      (j, drop, cut) in O(1): normal return, budget return, queue
+//      exhaustion or continue (_kernel.py:176-324)
+//   P4 group scan of child counts over the flat list; children split into
+//      two flat subsequences, A (t_lo = parent t_lo: lower children and u/v
+//      upper children) and B (t-split upper children), each sorted by
+//      (t_lo, push order)
+//   P5 next-level layout (slot order); eviction of queries whose level
+//      outgrew the tier; deferral of queries that do not fit this round
+//      (their level re-runs: record updates are idempotent, the check count
+//      is rolled back)
+//   P6 every child computes its rank in its query's next level by binary
+//      search of the other subsequence (merge by rank); a query whose B run
+//      is not sorted (non-dyadic t_max) uses an exact O(n) rank count
+//   P7 commit; admission refills free slots from the tier's input queue.
+#pragma once
+
+namespace tccd {
+
+constexpr uint8_t kPNone = 0xFF;
+constexpr int kIntMax = 0x7fffffff;
+constexpr uint8_t kClassified = 64;  // flag bit: box already classified
+
+// reference encoding
+constexpr unsigned kRefSrcMask = (1u << 29) - 1;  // position in the previous box array
+constexpr unsigned kRefCb = 1u << 29;             // upper child
+constexpr unsigned kRefSelf = 1u << 30;           // the box itself (deferred level)
+constexpr unsigned kRefRoot = 1u << 31;           // the query's root box
+
+struct Rec {  // first / drop record of a slot
+  Box b;
+  double codom;
+  int level;
+  int pad;
+};
+
+template <int G_, int NT_, int Q_, int CAP_, int QCAP_, int ADMIT_, bool SMEM_, int MINB_>
+struct EngineCfg {
+  static constexpr int G = G_;          // threads per independent group (32 = warp)
+  static constexpr int NT = NT_;        // threads per CTA (NT / G groups)
+  static constexpr int Q = Q_;          // query slots per group
+  static constexpr int CAP = CAP_;      // boxes per level list (0: runtime)
+  static constexpr int QCAP = QCAP_;    // largest per-query level (0: = cap)
+  static constexpr int ADMIT = ADMIT_;  // admit below this fill (0: = cap)
+  static constexpr bool SMEM = SMEM_;   // per-box bookkeeping in shared memory
+  static constexpr int MINB = MINB_;    // CTAs per SM (launch bounds)
+  using Off = typename std::conditional<(CAP_ > 0 && CAP_ <= 32768), unsigned short,
+                                        unsigned int>::type;
+};
+
+template <int G>
+__device__ __forceinline__ void gsync() {
+  if constexpr (G == 32) __syncwarp();
+  else __syncthreads();
+}
+
+// exclusive scan over a group (warp: shuffles; CTA: block scan)
+template <int G>
+__device__ __forceinline__ unsigned long long group_excl_scan(unsigned long long v,
+                                                              unsigned long long* sw,
+                                                              unsigned long long& total) {
+  if constexpr (G == 32) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+  } else {
+    return block_excl_scan<G>(v, sw, total);
+  }
+}
+
+// global arena of one group
+template <class Cfg>
+struct EngineArena {
+  using Off = typename Cfg::Off;
+  Box* box[2];
+  double* wb[2];
+  unsigned int* ref[2];
+  unsigned long long* akey;  // [2 cap]
+  unsigned int* apush;
+  unsigned int* aref;
+  unsigned long long* bkey;  // [cap]
+  unsigned int* bpush;
+  unsigned int* bref;
+  // per-box bookkeeping when it lives in global memory
+  uint8_t* slot_of[2];
+  uint8_t* flag[2];
+  Off* offA;
+  Off* offB;
+
+  __host__ __device__ static size_t bytes(long long cap) {
+    size_t b = 2 * align256(cap * sizeof(Box)) + 2 * align256(cap * 8) + 2 * align256(cap * 4) +
+               align256(2 * cap * 8) + 2 * align256(2 * cap * 4) + align256(cap * 8) +
+               2 * align256(cap * 4);
+    if (!Cfg::SMEM) b += 4 * align256(cap) + 2 * align256(cap * sizeof(Off));
+    return b;
+  }
+
+  __device__ void init(unsigned char* base, long long cap) {
+    size_t o = 0;
+    for (int k = 0; k < 2; ++k) { box[k] = (Box*)(base + o); o += align256(cap * sizeof(Box)); }
+    for (int k = 0; k < 2; ++k) { wb[k] = (double*)(base + o); o += align256(cap * 8); }
+    for (int k = 0; k < 2; ++k) { ref[k] = (unsigned int*)(base + o); o += align256(cap * 4); }
+    akey = (unsigned long long*)(base + o); o += align256(2 * cap * 8);
+    apush = (unsigned int*)(base + o); o += align256(2 * cap * 4);
+    aref = (unsigned int*)(base + o); o += align256(2 * cap * 4);
+    bkey = (unsigned long long*)(base + o); o += align256(cap * 8);
+    bpush = (unsigned int*)(base + o); o += align256(cap * 4);
+    bref = (unsigned int*)(base + o); o += align256(cap * 4);
+    if (!Cfg::SMEM) {
+      for (int k = 0; k < 2; ++k) { slot_of[k] = base + o; o += align256(cap); }
+      for (int k = 0; k < 2; ++k) { flag[k] = base + o; o += align256(cap); }
+      offA = (Off*)(base + o); o += align256(cap * sizeof(Off));
+      offB = (Off*)(base + o); o += align256(cap * sizeof(Off));
+    }
+  }
+};
+
+template <class Cfg>
+struct EngineShared {
+  static constexpr int Q = Cfg::Q;
+  double P[Q][24];
+  QueryParams qp[Q];
+  Rec rec[Q][2];         // [0] first, [1] drop
+  long long C[Q];        // checks before the current level
+  long long qidx[Q];     // -1: free slot
+  double root_wb[Q];
+  int level[Q];
+  int seg_off[Q], seg_n[Q];
+  int j[Q], acc[Q];
+  int segA0[Q], segB0[Q], segA1[Q], segB1[Q];
+  int next_off[Q];
+  int tot[Q];
+  uint8_t root_flag[Q];
+  uint8_t have_first[Q], have_drop[Q];
+  uint8_t cont[Q];       // 1: children kept; 2: deferred; 3: evicted (children counted)
+  uint8_t unsorted[Q];
+  unsigned long long sw[Cfg::G / 32];
+  int n_cur, n_next, admit_k, exhausted, A_tot, B_tot, rot;
+  unsigned long long deferred;
+  long long admit_base;
+  unsigned int free_mask[(Q + 31) / 32];
+};
+
+template <class Cfg>
+struct EngineSmemBoxes {
+  static constexpr int CAP = Cfg::SMEM ? Cfg::CAP : 1;
+  uint8_t slot_of[2][CAP];
+  uint8_t flag[2][CAP];
+  typename Cfg::Off offA[CAP], offB[CAP];
+};
+
+// shared memory of ONE group (16-byte aligned); a CTA holds NT / G groups
+template <class Cfg>
+__host__ __device__ constexpr size_t engine_smem_bytes() {
+  return (sizeof(EngineShared<Cfg>) + (Cfg::SMEM ? sizeof(EngineSmemBoxes<Cfg>) : 0) + 15) & ~size_t(15);
+}
+
+// split dimension and midpoint of a box that is refined (_kernel.py:219-241)
+__device__ __forceinline__ int split_dim(const Box& b, const double* kap, double& mid) {
+  const double ct = (b.t1 - b.t0) * kap[0];
+  const double cu = (b.u1 - b.u0) * kap[1];
+  const double cv = (b.v1 - b.v0) * kap[2];
+  int sdim = 0;
+  double best = ct;
+  if (cu > best) { sdim = 1; best = cu; }
+  if (cv > best) { sdim = 2; }
+  const double lo = sdim == 0 ? b.t0 : (sdim == 1 ? b.u0 : b.v0);
+  const double hi = sdim == 0 ? b.t1 : (sdim == 1 ? b.u1 : b.v1);
+  mid = 0.5 * (lo + hi);
+  return sdim;
+}
+
+struct TierIO {
+  const Pre* in;            // input queue
+  unsigned long long* in_count;
+  unsigned long long* in_next;
+  Pre* out;                 // eviction queue of the next tier (nullptr: none)
+  unsigned long long* out_count;
+  unsigned char* arenas;
+  size_t arena_bytes;
+  long long cap;            // boxes per level list
+  unsigned long long* rounds;
+  unsigned long long* deferred;
+  unsigned long long* evicted;
+  unsigned long long* boxes;
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, TierIO io) {
+  // Each group of G threads runs an independent engine instance with its own
+  // shared-memory state and global arena; groups never synchronize with one
+  // another (G = 32: warp-synchronous, no block barriers).
+  constexpr int G = Cfg::G, Q = Cfg::Q;
+  constexpr int NT = G;  // stride of the per-group loops
+  using Off = typename Cfg::Off;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int group = threadIdx.x / G;
+  unsigned char* gsmem = smem_raw + (size_t)group * engine_smem_bytes<Cfg>();
+  EngineShared<Cfg>& S = *reinterpret_cast<EngineShared<Cfg>*>(gsmem);
+  EngineArena<Cfg> ar;
+  ar.init(io.arenas + ((size_t)blockIdx.x * (Cfg::NT / G) + group) * io.arena_bytes, io.cap);
+  uint8_t* slot_of[2];
+  uint8_t* flags[2];
+  Off* offA;
+  Off* offB;
+  if (Cfg::SMEM) {
+    auto* SB = reinterpret_cast<EngineSmemBoxes<Cfg>*>(gsmem + sizeof(EngineShared<Cfg>));
+    slot_of[0] = SB->slot_of[0]; slot_of[1] = SB->slot_of[1];
+    flags[0] = SB->flag[0]; flags[1] = SB->flag[1];
+    offA = SB->offA; offB = SB->offB;
+  } else {
+    slot_of[0] = ar.slot_of[0]; slot_of[1] = ar.slot_of[1];
+    flags[0] = ar.flag[0]; flags[1] = ar.flag[1];
+    offA = ar.offA; offB = ar.offB;
+  }
+  const int cap = Cfg::CAP ? Cfg::CAP : (int)io.cap;
+  const int qcap = Cfg::QCAP ? Cfg::QCAP : cap;
+  const int admit_lim = Cfg::ADMIT ? Cfg::ADMIT : cap;
+  const unsigned long long in_total = *(volatile unsigned long long*)io.in_count;
+  const int tid = threadIdx.x % G;  // rank within the group
+  for (int s = tid; s < Q; s += NT) S.qidx[s] = -1;
+  if (tid == 0) { S.n_cur = 0; S.exhausted = 0; S.rot = 0; S.deferred = 0; }
+  gsync<G>();
+  int cur = 0;
+  long long rounds = 0;
+  unsigned long long evicted = 0, boxes = 0;
+
+  auto evict = [&](int s) {
+    const unsigned long long h = atomicAdd(io.out_count, 1ull);
+    Pre& p = io.out[h];
+    p.q = S.qidx[s];
+    for (int k = 0; k < 3; ++k) { p.eps[k] = S.qp[s].eps[k]; p.kap[k] = S.qp[s].kap[k]; }
+    p.wb = 0.0;
+    p.flag = 0;
+    S.qidx[s] = -1;
+    S.cont[s] = 3;
+    ++evicted;
+  };
+  auto finish = [&](int s, bool early, long long checks) {
+    // report min(drop, first) (_kernel.py:192-199, 208-213)
+    const bool use_drop =
+        S.have_drop[s] && (!S.have_first[s] || S.rec[s][1].b.t0 < S.rec[s][0].b.t0);
+    const Rec& r = S.rec[s][use_drop ? 1 : 0];
+    write_result(a, S.qidx[s], kHit, r.b, r.codom, checks, early, r.level);
+  };
+  auto free_result = [&](int s, long long checks) {
+    const Box z = {0, 0, 0, 0, 0, 0};
+    write_result(a, S.qidx[s], kFree, z, 0.0, checks, 0, 0);
+  };
+
+  for (;;) {
+    const int prv = cur ^ 1;
+    // ================= P0: admission
+    if (tid < 32) {
+      unsigned int cnt = 0;
+      for (int w = 0; w < (Q + 31) / 32; ++w) {
+        const int s = w * 32 + tid;
+        const unsigned int m = __ballot_sync(0xffffffffu, s < Q && S.qidx[s] < 0);
+        if (tid == 0) S.free_mask[w] = m;
+        cnt += __popc(m);
+      }
+      if (tid == 0) {
+        int k = (int)cnt;
+        int room = admit_lim - S.n_cur;
+        if (room < 0) room = 0;
+        if (k > room) k = room;
+        // fair share of what is left, so a short queue spreads over all groups
+        const unsigned long long taken = *(volatile unsigned long long*)io.in_next;
+        const unsigned long long left = taken < in_total ? in_total - taken : 0ull;
+        const unsigned long long groups = (unsigned long long)gridDim.x * (Cfg::NT / G);
+        const long long share = (long long)((left + groups - 1) / groups);
+        if (k > share) k = (int)(share > 0 ? share : 1);
+        long long base = 0;
+        if (S.exhausted) k = 0;
+        if (k > 0) {
+          base = (long long)atomicAdd(io.in_next, (unsigned long long)k);
+          if ((unsigned long long)base >= in_total) { k = 0; S.exhausted = 1; }
+          else if ((unsigned long long)(base + k) >= in_total) {
+            k = (int)(in_total - base);
+            S.exhausted = 1;
+          }
+        }
+        S.admit_k = k;
+        S.admit_base = base;
+      }
+    }
+    gsync<G>();
+    const int k_adm = S.admit_k;
+    for (int s = tid; s < Q; s += NT) {
+      if (S.qidx[s] < 0 && k_adm > 0) {
+        const int w = s >> 5, lane = s & 31;
+        int r = __popc(S.free_mask[w] & ((1u << lane) - 1u));
+        for (int ww = 0; ww < w; ++ww) r += __popc(S.free_mask[ww]);
+        if (r < k_adm) {
+          const Pre& pre = io.in[S.admit_base + r];
+          const long long q = pre.q;
+          const int pos = S.n_cur + r;
+          double* P = S.P[s];
+          const double* src = a.points + 24 * q;
+#pragma unroll
+          for (int i = 0; i < 24; i += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(src + i);
+            P[i] = v.x;
+            P[i + 1] = v.y;
+          }
+          QueryParams& qp = S.qp[s];
+          load_params(a, q, qp);
+          for (int k = 0; k < 3; ++k) { qp.eps[k] = pre.eps[k]; qp.kap[k] = pre.kap[k]; }
+          S.qidx[s] = q;
+          S.C[s] = 0;
+          S.level[s] = 0;
+          S.have_first[s] = 0;
+          S.have_drop[s] = 0;
+          S.seg_off[s] = pos;
+          S.seg_n[s] = 1;
+          S.root_flag[s] = (uint8_t)pre.flag;
+          S.root_wb[s] = pre.wb;
+          ar.ref[cur][pos] = kRefRoot;
+          slot_of[cur][pos] = (uint8_t)s;
+          flags[cur][pos] = (uint8_t)pre.flag;
+        }
+      }
+      S.j[s] = kIntMax;
+      S.acc[s] = kIntMax;
+      S.cont[s] = 0;
+      S.unsorted[s] = 0;
+    }
+    gsync<G>();
+    if (tid == 0) S.n_cur += k_adm;
+    gsync<G>();
+    const int n = S.n_cur;
+    if (n == 0) break;
+    ++rounds;
+    boxes += (unsigned long long)n;
+    Box* const bx = ar.box[cur];
+    const Box* const bprev = ar.box[prv];
+    double* const wbc = ar.wb[cur];
+    const double* const wbp = ar.wb[prv];
+    const unsigned int* const rf = ar.ref[cur];
+    uint8_t* const sl = slot_of[cur];
+    uint8_t* const fl = flags[cur];
+    // ================= P1: materialize + classify
+    for (int i = tid; i < n; i += NT) {
+      const int s = sl[i];
+      if (s == kPNone) continue;
+      const QueryParams& qp = S.qp[s];
+      const unsigned int r = rf[i];
+      Box b;
+      uint8_t f = 0;
+      double wb = 0.0;
+      if (r & kRefRoot) {
+        b = Box{0.0, qp.t_max, 0.0, 1.0, 0.0, 1.0};
+        f = fl[i];
+        wb = S.root_wb[s];
+      } else {
+        const int src = (int)(r & kRefSrcMask);
+        const Box p = bprev[src];
+        if (r & kRefSelf) {
+          b = p;
+          f = fl[i];
+          if ((f & kClassified) && (f & 3) != kDisjoint) wb = wbp[src];
+        } else {
+          double mid;
+          const int sdim = split_dim(p, qp.kap, mid);
+          Box c0, c1;
+          children(p, sdim, mid, c0, c1);
+          b = (r & kRefCb) ? c1 : c0;
+        }
+      }
+      bx[i] = b;
+      const int k = i - S.seg_off[s];
+      if (!(f & kClassified)) {
+        const long long cut = qp.max_checks - S.C[s] - 1;
+        if (k <= cut) {
+          const int cls = classify((const double*)S.P[s], qp.kind, b, qp.eps, qp.sep, wb);
+          f = (uint8_t)cls;
+          if (cls != kDisjoint) {
+            int sdim; double mid; bool ph;
+            const bool acc = split_decision(b, cls, wb, qp.kap, qp.delta, qp.kind, sdim, mid, ph);
+            f = make_flag(cls, acc, sdim, ph);
+          }
+          f |= kClassified;
+        }
+      }
+      if ((f & 3) != kDisjoint) {
+        wbc[i] = wb;
+        atomicMin(&S.j[s], k);
+      }
+      fl[i] = f;
+    }
+    gsync<G>();
+    // ================= P2: first accepted box after j, before the cut
+    for (int i = tid; i < n; i += NT) {
+      const int s = sl[i];
+      if (s == kPNone) continue;
+      const int k = i - S.seg_off[s];
+      if (k <= S.j[s]) continue;
+      const long long cut = S.qp[s].max_checks - S.C[s] - 1;
+      const long long eend = S.seg_n[s] < cut ? S.seg_n[s] : cut;
+      if (k >= eend) continue;
+      const uint8_t f = fl[i];
+      if ((f & 3) != kDisjoint && (f & 4)) atomicMin(&S.acc[s], k);
+    }
+    gsync<G>();
+    // ================= P3: per-query outcome (O(1) replay of the level's events)
+    for (int s = tid; s < Q; s += NT) {
+      if (S.qidx[s] < 0) continue;
+      const int nn = S.seg_n[s];
+      const long long C = S.C[s], mc = S.qp[s].max_checks;
+      const long long cut = mc - C - 1;
+      const long long ecls = nn < cut + 1 ? nn : cut + 1;
+      const int j = S.j[s];
+      bool done = true;
+      if (j >= ecls) {
+        if (cut < nn) {
+          if (S.have_drop[s] || cut + 1 < nn) finish(s, true, mc);
+          else free_result(s, mc);
+        } else if (S.have_drop[s]) {
+          const Rec& r = S.rec[s][1];
+          write_result(a, S.qidx[s], kHit, r.b, r.codom, C + nn, 0, r.level);
+        } else {
+          free_result(s, C + nn);
+        }
+      } else {
+        const int ij = S.seg_off[s] + j;
+        const Box bj = bx[ij];
+        const double wbj = wbc[ij];
+        Rec& fr = S.rec[s][0];
+        fr.b = bj;
+        fr.codom = wbj;
+        fr.level = S.level[s];
+        S.have_first[s] = 1;
+        if (j == cut) {
+          finish(s, true, mc);
+        } else if (fl[ij] & 4) {
+          // first colliding box of a fresh level accepted (_kernel.py:243-252)
+          if (S.have_drop[s] && S.rec[s][1].b.t0 < bj.t0) {
+            const Rec& r = S.rec[s][1];
+            write_result(a, S.qidx[s], kHit, r.b, r.codom, C + j + 1, 0, r.level);
+          } else {
+            write_result(a, S.qidx[s], kHit, bj, wbj, C + j + 1, 0, S.level[s]);
+          }
+        } else {
+          const long long eend = nn < cut ? nn : cut;
+          const int ai = S.acc[s];
+          if (ai < eend) {
+            const Box ba = bx[S.seg_off[s] + ai];
+            if (!S.have_drop[s] || ba.t0 < S.rec[s][1].b.t0) {
+              Rec& dr = S.rec[s][1];
+              dr.b = ba;
+              dr.codom = wbc[S.seg_off[s] + ai];
+              dr.level = S.level[s];
+            }
+            S.have_drop[s] = 1;
+          }
+          if (cut < nn) {
+            finish(s, true, mc);
+          } else {
+            done = false;
+            S.cont[s] = 1;
+            S.C[s] = C + nn;
+          }
+        }
+      }
+      if (done) S.qidx[s] = -1;
+    }
+    gsync<G>();
+    // ================= P4: child counts -> flat A / B positions
+    {
+      const int c = (n + NT - 1) / NT;
+      const int lo = tid * c;
+      const int hi = lo + c < n ? lo + c : n;
+      unsigned int sA = 0, sB = 0;
+      for (int i = lo; i < hi; ++i) {
+        const int s = sl[i];
+        if (s == kPNone || !S.cont[s]) continue;
+        if (i - S.seg_off[s] < S.j[s]) continue;
+        const uint8_t f = fl[i];
+        if ((f & 3) == kDisjoint || (f & 4)) continue;
+        const int sdim = (f >> 3) & 3;
+        sA += 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
+        sB += sdim == 0 ? 1 : 0;
+      }
+      unsigned long long tot;
+      const unsigned long long pre =
+          group_excl_scan<G>(((unsigned long long)sA << 32) | sB, S.sw, tot);
+      unsigned int Ar = (unsigned int)(pre >> 32), Br = (unsigned int)(pre & 0xffffffffu);
+      if (tid == 0) { S.A_tot = (int)(tot >> 32); S.B_tot = (int)(tot & 0xffffffffu); }
+      for (int i = lo; i < hi; ++i) {
+        const int s = sl[i];
+        if (s == kPNone) continue;
+        const int k = i - S.seg_off[s];
+        if (k == 0) { S.segA0[s] = (int)Ar; S.segB0[s] = (int)Br; }
+        offA[i] = (Off)Ar;
+        offB[i] = (Off)Br;
+        if (S.cont[s] && k >= S.j[s]) {
+          const uint8_t f = fl[i];
+          if ((f & 3) != kDisjoint && !(f & 4)) {
+            const int sdim = (f >> 3) & 3;
+            Ar += 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
+            Br += sdim == 0 ? 1 : 0;
+          }
+        }
+        if (k == S.seg_n[s] - 1) { S.segA1[s] = (int)Ar; S.segB1[s] = (int)Br; }
+      }
+    }
+    gsync<G>();
+    // ================= P5: next-level layout (slot order), eviction, deferral
+    // Levels above the tier's per-query cap go to the next tier.  Otherwise
+    // the first K slots (rotating order) keep their children and the rest
+    // are deferred, K = the largest k with
+    //   sum_{r<k} children_r + sum_{r>=k} boxes_r <= cap
+    // (at least one query advances: if none fits, the first is evicted).
+    for (int s = tid; s < Q; s += NT) {
+      int t = 0;
+      if (S.cont[s]) {
+        t = (S.segA1[s] - S.segA0[s]) + (S.segB1[s] - S.segB0[s]);
+        if (t > qcap) evict(s);
+      }
+      S.tot[s] = t;
+    }
+    gsync<G>();
+    if (tid < 32) {
+      const int lane = tid;
+      constexpr int kPer = (Q + 31) / 32;
+      int vt[kPer], vn[kPer];
+      int st, sn, it, in, Nn, K;
+      for (;;) {
+        st = 0; sn = 0;
+#pragma unroll
+        for (int m = 0; m < kPer; ++m) {
+          const int rpos = lane * kPer + m;
+          const int s = (S.rot + rpos) % Q;
+          const bool ok = rpos < Q && S.cont[s] == 1;
+          vt[m] = ok ? S.tot[s] : 0;
+          vn[m] = ok ? S.seg_n[s] : 0;
+          st += vt[m];
+          sn += vn[m];
+        }
+        it = st; in = sn;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int yt = __shfl_up_sync(0xffffffffu, it, o);
+          const int yn = __shfl_up_sync(0xffffffffu, in, o);
+          if (lane >= o) { it += yt; in += yn; }
+        }
+        Nn = __shfl_sync(0xffffffffu, in, 31);
+        int pt = it - st, pn = in - sn;
+        int bestk = 0;
+#pragma unroll
+        for (int m = 0; m < kPer; ++m) {
+          pt += vt[m];
+          pn += vn[m];
+          if (vn[m] > 0 && pt + (Nn - pn) <= cap) bestk = lane * kPer + m + 1;
+        }
+        K = bestk;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) K = max(K, __shfl_xor_sync(0xffffffffu, K, o));
+        if (K > 0 || Nn == 0) break;
+        const unsigned int has = __ballot_sync(0xffffffffu, sn > 0);
+        if (lane == __ffs(has) - 1) {
+#pragma unroll
+          for (int m = 0; m < kPer; ++m) {
+            const int rpos = lane * kPer + m;
+            const int s = (S.rot + rpos) % Q;
+            if (vn[m] > 0) { evict(s); break; }
+          }
+        }
+        __syncwarp();
+      }
+      int cT = 0, cN = 0;
+#pragma unroll
+      for (int m = 0; m < kPer; ++m)
+        if (lane * kPer + m < K) { cT += vt[m]; cN += vn[m]; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        cT += __shfl_xor_sync(0xffffffffu, cT, o);
+        cN += __shfl_xor_sync(0xffffffffu, cN, o);
+      }
+      int ut = it - st, un = in - sn;
+      int deferred = 0;
+#pragma unroll
+      for (int m = 0; m < kPer; ++m) {
+        const int rpos = lane * kPer + m;
+        const int s = (S.rot + rpos) % Q;
+        if (rpos < Q && S.cont[s] == 1) {
+          if (rpos < K) {
+            S.next_off[s] = ut;
+          } else {
+            S.next_off[s] = cT + (un - cN);
+            S.cont[s] = 2;
+            ++deferred;
+          }
+        }
+        ut += vt[m];
+        un += vn[m];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) deferred += __shfl_xor_sync(0xffffffffu, deferred, o);
+      if (lane == 0) {
+        S.n_next = cT + (Nn - cN);
+        S.rot = (S.rot + 1) % Q;
+        S.deferred += deferred;
+      }
+    }
+    gsync<G>();
+    // ================= P5b: A / B entries (key, push, ref); deferred carry-over
+    const int nxt = prv;
+    for (int i = tid; i < n; i += NT) {
+      const int s = sl[i];
+      if (s == kPNone) continue;
+      const int k = i - S.seg_off[s];
+      if (S.cont[s] == 2) {
+        const int pos = S.next_off[s] + k;
+        ar.ref[nxt][pos] = (unsigned)i | kRefSelf;
+        slot_of[nxt][pos] = (uint8_t)s;
+        flags[nxt][pos] = fl[i];
+      }
+      // entries are written for every query counted in P4 (kept, deferred or
+      // evicted) so that no stale entry sits inside the flat A / B ranges
+      if (S.cont[s] == 0 || k < S.j[s]) continue;
+      const uint8_t f = fl[i];
+      if ((f & 3) == kDisjoint || (f & 4)) continue;
+      const int sdim = (f >> 3) & 3;
+      const Box b = bx[i];
+      const unsigned int oa = offA[i], ob = offB[i];
+      const unsigned int push = oa + ob;
+      const unsigned long long k0 = tkey(b.t0);
+      ar.akey[oa] = k0;
+      ar.apush[oa] = push;
+      ar.aref[oa] = (unsigned)i;
+      if (sdim != 0) {
+        if (f & 32) {
+          ar.akey[oa + 1] = k0;
+          ar.apush[oa + 1] = push + 1;
+          ar.aref[oa + 1] = (unsigned)i | kRefCb;
+        }
+      } else {
+        ar.bkey[ob] = tkey(0.5 * (b.t0 + b.t1));
+        ar.bpush[ob] = push + 1;
+        ar.bref[ob] = (unsigned)i | kRefCb;
+      }
+    }
+    gsync<G>();
+    // B runs sorted?  (always, for dyadic t_max)
+    {
+      const int B_tot = S.B_tot;
+      for (int b = tid + 1; b < B_tot; b += NT) {
+        const int s = sl[ar.bref[b] & kRefSrcMask];
+        if (S.cont[s] != 1 || b <= S.segB0[s]) continue;
+        if (ar.bkey[b - 1] > ar.bkey[b]) S.unsorted[s] = 1;
+      }
+    }
+    gsync<G>();
+    // ================= P6: merge by rank into the next level's reference list
+    {
+      const int A_tot = S.A_tot, B_tot = S.B_tot;
+      unsigned int* out = ar.ref[nxt];
+      uint8_t* sln = slot_of[nxt];
+      uint8_t* fln = flags[nxt];
+      for (int e = tid; e < A_tot + B_tot; e += NT) {
+        const bool isA = e < A_tot;
+        const int x = isA ? e : e - A_tot;
+        const unsigned int r = isA ? ar.aref[x] : ar.bref[x];
+        const int s = sl[r & kRefSrcMask];
+        if (S.cont[s] != 1) continue;
+        const unsigned long long kk = isA ? ar.akey[x] : ar.bkey[x];
+        const unsigned int pp = isA ? ar.apush[x] : ar.bpush[x];
+        int rank;
+        if (!S.unsorted[s]) {
+          if (isA) {
+            int l = S.segB0[s], h = S.segB1[s];  // B elements < (kk, pp)
+            while (l < h) {
+              const int m = (l + h) >> 1;
+              if (kp_less(ar.bkey[m], ar.bpush[m], kk, pp)) l = m + 1;
+              else h = m;
+            }
+            rank = (x - S.segA0[s]) + (l - S.segB0[s]);
+          } else {
+            int l = S.segA0[s], h = S.segA1[s];  // A elements < (kk, pp)
+            while (l < h) {
+              const int m = (l + h) >> 1;
+              if (kp_less(ar.akey[m], ar.apush[m], kk, pp)) l = m + 1;
+              else h = m;
+            }
+            rank = (x - S.segB0[s]) + (l - S.segA0[s]);
+          }
+        } else {
+          // exact rank count over the query's children (general t_max)
+          rank = 0;
+          for (int m = S.segA0[s]; m < S.segA1[s]; ++m)
+            rank += kp_less(ar.akey[m], ar.apush[m], kk, pp) ? 1 : 0;
+          for (int m = S.segB0[s]; m < S.segB1[s]; ++m)
+            rank += kp_less(ar.bkey[m], ar.bpush[m], kk, pp) ? 1 : 0;
+        }
+        const int pos = S.next_off[s] + rank;
+        out[pos] = r;
+        sln[pos] = (uint8_t)s;
+        fln[pos] = 0;
+      }
+    }
+    gsync<G>();
+    // ================= P7: commit
+    for (int s = tid; s < Q; s += NT) {
+      if (S.cont[s] == 1) {
+        S.seg_n[s] = S.tot[s];
+        S.level[s] += 1;
+        S.seg_off[s] = S.next_off[s];
+      } else if (S.cont[s] == 2) {
+        S.C[s] -= S.seg_n[s];  // the level re-runs next round
+        S.seg_off[s] = S.next_off[s];
+      }
+    }
+    gsync<G>();
+    if (tid == 0) S.n_cur = S.n_next;
+    cur = nxt;
+    gsync<G>();
+  }
+  if (tid == 0) {
+    atomicAdd(io.rounds, (unsigned long long)rounds);
+    atomicAdd(io.deferred, S.deferred);
+    atomicAdd(io.boxes, boxes);
+  }
+  if (evicted) atomicAdd(io.evicted, evicted);
+}
+
+}  // namespace tccd

@@ -44,8 +44,23 @@ def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
     return (n * rank) // world, (n * (rank + 1)) // world
 
 
-def default_heavy_blocks(device: torch.device) -> int:
+def sm_count(device: torch.device) -> int:
     return torch.cuda.get_device_properties(device).multi_processor_count
+
+
+def default_heavy_blocks(device: torch.device, n: int = 1, max_checks_max: int = 1) -> int:
+    """Giant-tier CTAs: one per SM, fewer if their 2*m_I-box arenas would take
+    more than half of the free device memory."""
+    sms = sm_count(device)
+    lib = _lib.lib()
+    base = int(lib.tccd_workspace_bytes(int(n), int(max_checks_max), 1))
+    per = int(lib.tccd_workspace_bytes(int(n), int(max_checks_max), 2)) - base
+    if per <= 0:
+        return sms
+    free, _ = torch.cuda.mem_get_info(device)
+    cached = sum(w.numel() for (t, i), w in _workspaces.items() if i == device.index)
+    budget = (free + cached) // 2 - base
+    return max(1, min(sms, int(budget // per)))
 
 
 def workspace_bytes(n: int, max_checks_max: int, heavy_blocks: int) -> int:
@@ -148,10 +163,10 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
     if "early" in want: out["early"] = torch.empty(n, dtype=torch.uint8, device=dev)
     if "witness" in want: out["witness"] = torch.empty((n, 6), dtype=torch.float64, device=dev)
     if "level" in want: out["level"] = torch.empty(n, dtype=torch.int32, device=dev)
-    st = torch.zeros(4, dtype=torch.int64, device=dev) if stats else None
+    st = torch.zeros(8, dtype=torch.int64, device=dev) if stats else None
 
-    hb = heavy_blocks or default_heavy_blocks(dev)
     with torch.cuda.device(dev):
+        hb = heavy_blocks or default_heavy_blocks(dev, n, mc_max)
         nbytes = workspace_bytes(n, mc_max, hb)
         ws = _workspace(dev, nbytes)
         b = _lib.TccdBatch()
@@ -176,7 +191,7 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
         b.workspace = _ptr(ws)
         b.workspace_bytes = ws.numel()
         b.heavy_blocks = hb
-        b.device_sms = default_heavy_blocks(dev)
+        b.device_sms = sm_count(dev)
         b.stats = _ptr(st)
         stream = torch.cuda.current_stream(dev)
         rc = lib.tccd_solve_batch(ctypes.byref(b), ctypes.c_void_p(stream.cuda_stream))

@@ -37,4 +37,5 @@ for r in range(args.reps):
     torch.cuda.synchronize()
     st = out["stats"].tolist()
     print(f"rep {r}: {e0.elapsed_time(e1):.2f} ms  checks {int(out['checks'].sum())} "
-          f"evicted {st[0]} rounds {st[1]} deferrals {st[2]}", flush=True)
+          f"giant {st[0]} medium {st[3]} rounds {st[1]} deferrals {st[2]} "
+          f"boxes L/M/G {st[4]}/{st[5]}/{st[6]}", flush=True)
