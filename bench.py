@@ -43,6 +43,7 @@ import numpy as np  # noqa: E402
 F_CHECK = {0: 200, 1: 174}
 P_QUERY = {0: 248, 1: 222}
 METRIC = "CCD queries/sec (FP64, delta=1e-6) at 1/2/4/8 B200; % of FP64 roofline"
+LAUNCHES_PER_SOLVE = 4  # per 2^22-query chunk: prologue + light + medium + giant engine
 
 
 def algorithmic_flops(kind: np.ndarray, checks: np.ndarray) -> float:
@@ -230,7 +231,7 @@ def main():
     full = solve_batch(pts, kind, device=dev, stats=True, **kw)
     checks = full["checks"].cpu().numpy()
     hits = int((full["status"] == 1).sum().item())
-    evicted = int(full["stats"][0].item())
+    evicted = int(full["stats"][0].item())  # queries that reached the giant tier
     pool_rounds = int(full["stats"][1].item())
     deferrals = int(full["stats"][2].item())
     flops = algorithmic_flops(w.kind, checks)
@@ -299,13 +300,16 @@ def main():
                      "peak_source": "measured on this box: DFMA probe (libtccd_probe.so), FMA-counted",
                      "fma_free_ceiling_tflops": peaks["dadd_tflops"],
                      "flops_per_step": flops,
-                     "kernels": "light_kernel + heavy_kernel (one solve)"},
+                     "kernels": "one solve = prologue_kernel + engine_kernel x3 tiers "
+                                 "(light / medium / giant), CUDA events on the launching stream"},
         "cpu_baseline": cpu,
         "clocks": clk,
-        "gpu_launches": 2 * args.steps * 2,
+        "gpu_launches": 2 * args.steps * LAUNCHES_PER_SOLVE * ((Q + (1 << 22) - 1) >> 22),
         "workload_stats": {"hits": hits, "hit_rate": hits / Q, "mean_checks": float(checks.mean()),
-                           "max_checks": int(checks.max()), "evicted_to_block_engine": evicted,
-                           "pool_rounds": pool_rounds, "pool_deferrals": deferrals},
+                           "max_checks": int(checks.max()), "giant_tier_queries": evicted,
+                           "engine_rounds": pool_rounds, "level_deferrals": deferrals,
+                           "medium_tier_queries": int(full["stats"][3].item()),
+                           "boxes_per_tier": [int(x) for x in full["stats"][4:7].tolist()]},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
