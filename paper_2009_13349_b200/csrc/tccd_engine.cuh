@@ -43,6 +43,7 @@ namespace tccd {
 constexpr uint8_t kPNone = 0xFF;
 constexpr int kIntMax = 0x7fffffff;
 constexpr uint8_t kClassified = 64;  // flag bit: box already classified
+constexpr uint8_t kHead = 128;       // flag bit: first box of a run of equal t_lo
 
 // reference encoding
 constexpr unsigned kRefSrcMask = (1u << 29) - 1;  // position in the previous box array
@@ -94,6 +95,46 @@ __device__ __forceinline__ unsigned long long group_excl_scan(unsigned long long
     return x - v;
   } else {
     return block_excl_scan<G>(v, sw, total);
+  }
+}
+
+// exclusive scans of ints over a group: forward max, and reverse min (over
+// the ranks above this one)
+template <int G, bool REV, bool MAX>
+__device__ __forceinline__ int group_scan_excl_int(int v, int ident, int* swi) {
+  const int lane = threadIdx.x & 31;
+  auto op = [](int a, int b) { return MAX ? (a > b ? a : b) : (a < b ? a : b); };
+  int x = v;  // inclusive in scan direction
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = REV ? __shfl_down_sync(0xffffffffu, x, o) : __shfl_up_sync(0xffffffffu, x, o);
+    if (REV ? lane + o < 32 : lane >= o) x = op(x, y);
+  }
+  int ex = REV ? __shfl_down_sync(0xffffffffu, x, 1) : __shfl_up_sync(0xffffffffu, x, 1);
+  if (REV ? lane == 31 : lane == 0) ex = ident;
+  if constexpr (G == 32) {
+    return ex;
+  } else {
+    constexpr int NW = G / 32;
+    const int w = (threadIdx.x % G) >> 5;
+    if (REV ? lane == 0 : lane == 31) swi[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int t = lane < NW ? swi[lane] : ident;
+      int ti = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = REV ? __shfl_down_sync(0xffffffffu, ti, o) : __shfl_up_sync(0xffffffffu, ti, o);
+        if (REV ? lane + o < NW : lane >= o) ti = op(ti, y);
+      }
+      int te = REV ? __shfl_down_sync(0xffffffffu, ti, 1) : __shfl_up_sync(0xffffffffu, ti, 1);
+      if (REV ? lane == NW - 1 : lane == 0) te = ident;
+      if (lane < NW) swi[NW + lane] = te;  // exclusive prefix over warps
+    }
+    __syncthreads();
+    const int r = op(swi[NW + w], ex);
+    __syncthreads();
+    return r;
   }
 }
 
@@ -163,7 +204,11 @@ struct EngineShared {
   uint8_t have_first[Q], have_drop[Q];
   uint8_t cont[Q];       // 1: children kept; 2: deferred; 3: evicted (children counted)
   uint8_t unsorted[Q];
+  uint8_t uniform[Q];    // dyadic t_max: every level has uniform widths (closed-form order)
+  int segP0[Q];          // flat count of refining boxes before the segment
   unsigned long long sw[Cfg::G / 32];
+  int swi[2 * (Cfg::G / 32)];
+  int any_general;
   int n_cur, n_next, admit_k, exhausted, A_tot, B_tot, rot;
   unsigned long long deferred;
   long long admit_base;
@@ -344,9 +389,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           S.seg_n[s] = 1;
           S.root_flag[s] = (uint8_t)pre.flag;
           S.root_wb[s] = pre.wb;
+          int ex;
+          S.uniform[s] = frexp(qp.t_max, &ex) == 0.5;  // t_max a power of two
           ar.ref[cur][pos] = kRefRoot;
           slot_of[cur][pos] = (uint8_t)s;
-          flags[cur][pos] = (uint8_t)pre.flag;
+          flags[cur][pos] = (uint8_t)pre.flag | kHead;
         }
       }
       S.j[s] = kIntMax;
@@ -355,7 +402,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       S.unsorted[s] = 0;
     }
     gsync<G>();
-    if (tid == 0) S.n_cur += k_adm;
+    if (tid == 0) { S.n_cur += k_adm; S.any_general = 0; }
     gsync<G>();
     const int n = S.n_cur;
     if (n == 0) break;
@@ -375,18 +422,16 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       const QueryParams& qp = S.qp[s];
       const unsigned int r = rf[i];
       Box b;
-      uint8_t f = 0;
+      uint8_t f = fl[i];  // head bit (+ class, for roots and deferred boxes)
       double wb = 0.0;
       if (r & kRefRoot) {
         b = Box{0.0, qp.t_max, 0.0, 1.0, 0.0, 1.0};
-        f = fl[i];
         wb = S.root_wb[s];
       } else {
         const int src = (int)(r & kRefSrcMask);
         const Box p = bprev[src];
         if (r & kRefSelf) {
           b = p;
-          f = fl[i];
           if ((f & kClassified) && (f & 3) != kDisjoint) wb = wbp[src];
         } else {
           double mid;
@@ -401,6 +446,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       if (!(f & kClassified)) {
         const long long cut = qp.max_checks - S.C[s] - 1;
         if (k <= cut) {
+          const uint8_t head = f & kHead;
           const int cls = classify((const double*)S.P[s], qp.kind, b, qp.eps, qp.sep, wb);
           f = (uint8_t)cls;
           if (cls != kDisjoint) {
@@ -408,7 +454,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
             const bool acc = split_decision(b, cls, wb, qp.kap, qp.delta, qp.kind, sdim, mid, ph);
             f = make_flag(cls, acc, sdim, ph);
           }
-          f |= kClassified;
+          f |= kClassified | head;
         }
       }
       if ((f & 3) != kDisjoint) {
@@ -494,44 +540,66 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       if (done) S.qidx[s] = -1;
     }
     gsync<G>();
-    // ================= P4: child counts -> flat A / B positions
+    // ================= P4: child counts -> flat prefixes (A, B, refining boxes P)
+    // Threads own contiguous chunks.  For uniform queries (dyadic t_max) the
+    // next level's order is closed-form (see P4c); the run carries M (P at the
+    // head of the current run) and N (P at the next head) come from a
+    // forward max-scan and a reverse min-scan over the chunks.
+    const int c4 = (n + NT - 1) / NT;
+    const int lo4 = tid * c4;
+    const int hi4 = lo4 + c4 < n ? lo4 + c4 : n;
+    int P_end, A_end, carryN;
     {
-      const int c = (n + NT - 1) / NT;
-      const int lo = tid * c;
-      const int hi = lo + c < n ? lo + c : n;
       unsigned int sA = 0, sB = 0;
-      for (int i = lo; i < hi; ++i) {
+      int sP = 0, lastHeadP = -1, firstHeadP = -1;
+      bool general = false;
+      for (int i = lo4; i < hi4; ++i) {
         const int s = sl[i];
-        if (s == kPNone || !S.cont[s]) continue;
-        if (i - S.seg_off[s] < S.j[s]) continue;
+        if (s == kPNone) continue;
         const uint8_t f = fl[i];
+        if (f & kHead) { if (firstHeadP < 0) firstHeadP = sP; lastHeadP = sP; }
+        if (!S.cont[s]) continue;
+        general |= !S.uniform[s];
+        if (i - S.seg_off[s] < S.j[s]) continue;
         if ((f & 3) == kDisjoint || (f & 4)) continue;
         const int sdim = (f >> 3) & 3;
         sA += 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
         sB += sdim == 0 ? 1 : 0;
+        sP += 1;
       }
+      if (general) S.any_general = 1;
       unsigned long long tot;
       const unsigned long long pre =
           group_excl_scan<G>(((unsigned long long)sA << 32) | sB, S.sw, tot);
+      unsigned long long totP;
+      const int P0 = (int)group_excl_scan<G>((unsigned long long)sP, S.sw, totP);
+      const int carryM = group_scan_excl_int<G, false, true>(
+          lastHeadP >= 0 ? P0 + lastHeadP : -1, -1, S.swi);
+      carryN = group_scan_excl_int<G, true, false>(
+          firstHeadP >= 0 ? P0 + firstHeadP : kIntMax, kIntMax, S.swi);
+      if (carryN == kIntMax) carryN = (int)totP;
       unsigned int Ar = (unsigned int)(pre >> 32), Br = (unsigned int)(pre & 0xffffffffu);
+      int Pr = P0, M = carryM;
       if (tid == 0) { S.A_tot = (int)(tot >> 32); S.B_tot = (int)(tot & 0xffffffffu); }
-      for (int i = lo; i < hi; ++i) {
+      for (int i = lo4; i < hi4; ++i) {
         const int s = sl[i];
         if (s == kPNone) continue;
         const int k = i - S.seg_off[s];
-        if (k == 0) { S.segA0[s] = (int)Ar; S.segB0[s] = (int)Br; }
-        offA[i] = (Off)Ar;
+        const uint8_t f = fl[i];
+        if (f & kHead) M = Pr;
+        if (k == 0) { S.segA0[s] = (int)Ar; S.segB0[s] = (int)Br; S.segP0[s] = Pr; }
+        offA[i] = S.uniform[s] ? (Off)M : (Off)Ar;  // uniform: run-start carry
         offB[i] = (Off)Br;
-        if (S.cont[s] && k >= S.j[s]) {
-          const uint8_t f = fl[i];
-          if ((f & 3) != kDisjoint && !(f & 4)) {
-            const int sdim = (f >> 3) & 3;
-            Ar += 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
-            Br += sdim == 0 ? 1 : 0;
-          }
+        if (S.cont[s] && k >= S.j[s] && (f & 3) != kDisjoint && !(f & 4)) {
+          const int sdim = (f >> 3) & 3;
+          Ar += 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
+          Br += sdim == 0 ? 1 : 0;
+          Pr += 1;
         }
         if (k == S.seg_n[s] - 1) { S.segA1[s] = (int)Ar; S.segB1[s] = (int)Br; }
       }
+      P_end = Pr;
+      A_end = (int)Ar;
     }
     gsync<G>();
     // ================= P5: next-level layout (slot order), eviction, deferral
@@ -633,18 +701,74 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       }
     }
     gsync<G>();
-    // ================= P5b: A / B entries (key, push, ref); deferred carry-over
+    // ================= P4c: next level of uniform queries, closed form; deferred carry
+    // For dyadic t_max every box of a level has the same widths, hence the
+    // same split dimension.  u/v split: the children are already in stable
+    // t_lo order (push order).  t split: within a run of equal t_lo, all
+    // lower children (t_lo kept) then all upper children (t_lo + w/2, below
+    // the next run's t_lo), so with P = refining boxes before the parent,
+    // M / N = P at the run's head / at the next head:
+    //   rank(lower) = M + P,  rank(upper) = N + P   (segment-relative).
+    // New run heads: the children of the first refining box of a run.
     const int nxt = prv;
+    {
+      int Pr = P_end, Ar = A_end, N = carryN;
+      unsigned int* const outr = ar.ref[nxt];
+      uint8_t* const sln = slot_of[nxt];
+      uint8_t* const fln = flags[nxt];
+      for (int i = hi4 - 1; i >= lo4; --i) {
+        const int s = sl[i];
+        if (s == kPNone) continue;
+        const uint8_t f = fl[i];
+        const int k = i - S.seg_off[s];
+        const int cs = S.cont[s];
+        if (cs == 2) {
+          const int pos = S.next_off[s] + k;
+          outr[pos] = (unsigned)i | kRefSelf;
+          sln[pos] = (uint8_t)s;
+          fln[pos] = f;
+        }
+        if (cs != 0 && k >= S.j[s] && (f & 3) != kDisjoint && !(f & 4)) {
+          const int sdim = (f >> 3) & 3;
+          Pr -= 1;
+          Ar -= 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
+          if (cs == 1 && S.uniform[s]) {
+            const int M = (int)offA[i];
+            const int S0 = S.segP0[s];
+            const uint8_t hd = Pr == M ? kHead : 0;
+            const int base = S.next_off[s];
+            if (sdim == 0) {
+              const int rl = base + (M - S0) + (Pr - S0);
+              const int ru = base + (N - S0) + (Pr - S0);
+              outr[rl] = (unsigned)i;
+              sln[rl] = (uint8_t)s;
+              fln[rl] = hd;
+              outr[ru] = (unsigned)i | kRefCb;
+              sln[ru] = (uint8_t)s;
+              fln[ru] = hd;
+            } else {
+              const int rl = base + (Ar - S.segA0[s]);
+              outr[rl] = (unsigned)i;
+              sln[rl] = (uint8_t)s;
+              fln[rl] = hd;
+              if (f & 32) {
+                outr[rl + 1] = (unsigned)i | kRefCb;
+                sln[rl + 1] = (uint8_t)s;
+                fln[rl + 1] = 0;
+              }
+            }
+          }
+        }
+        if (f & kHead) N = Pr;
+      }
+    }
+    gsync<G>();
+    if (S.any_general) {
+    // ================= P5b: A / B entries (key, push, ref); deferred carry-over
     for (int i = tid; i < n; i += NT) {
       const int s = sl[i];
       if (s == kPNone) continue;
       const int k = i - S.seg_off[s];
-      if (S.cont[s] == 2) {
-        const int pos = S.next_off[s] + k;
-        ar.ref[nxt][pos] = (unsigned)i | kRefSelf;
-        slot_of[nxt][pos] = (uint8_t)s;
-        flags[nxt][pos] = fl[i];
-      }
       // entries are written for every query counted in P4 (kept, deferred or
       // evicted) so that no stale entry sits inside the flat A / B ranges
       if (S.cont[s] == 0 || k < S.j[s]) continue;
@@ -676,7 +800,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       const int B_tot = S.B_tot;
       for (int b = tid + 1; b < B_tot; b += NT) {
         const int s = sl[ar.bref[b] & kRefSrcMask];
-        if (S.cont[s] != 1 || b <= S.segB0[s]) continue;
+        if (S.cont[s] != 1 || S.uniform[s] || b <= S.segB0[s]) continue;
         if (ar.bkey[b - 1] > ar.bkey[b]) S.unsorted[s] = 1;
       }
     }
@@ -692,7 +816,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         const int x = isA ? e : e - A_tot;
         const unsigned int r = isA ? ar.aref[x] : ar.bref[x];
         const int s = sl[r & kRefSrcMask];
-        if (S.cont[s] != 1) continue;
+        if (S.cont[s] != 1 || S.uniform[s]) continue;
         const unsigned long long kk = isA ? ar.akey[x] : ar.bkey[x];
         const unsigned int pp = isA ? ar.apush[x] : ar.bpush[x];
         int rank;
@@ -729,6 +853,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       }
     }
     gsync<G>();
+    }  // any_general
     // ================= P7: commit
     for (int s = tid; s < Q; s += NT) {
       if (S.cont[s] == 1) {
