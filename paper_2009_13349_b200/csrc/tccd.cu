@@ -232,14 +232,22 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long
 namespace tccd {
 
 //                   G    NT   Q   CAP    QCAP   ADMIT  SMEM   MINB
-#ifndef TCCD_TIERS
-#define TCCD_TIERS 2
+#ifndef TCCD_LQ
+#define TCCD_LQ 64
 #endif
-#if TCCD_TIERS == 1
-using LightCfg = EngineCfg<256, 256, 128, 8192, 1024, 4096, true, 2>;
+#ifndef TCCD_LADMIT
+#define TCCD_LADMIT 2048
+#endif
+#ifndef TCCD_LQCAP
+#define TCCD_LQCAP 1024
+#endif
+#ifndef TCCD_MSMEM
+#define TCCD_MSMEM 1
+#endif
+using LightCfg = EngineCfg<256, 256, TCCD_LQ, 8192, TCCD_LQCAP, TCCD_LADMIT, true, 2>;
+#if TCCD_MSMEM
 using MediumCfg = EngineCfg<512, 512, 16, 16384, 8192, 8192, true, 1>;
 #else
-using LightCfg = EngineCfg<256, 256, 64, 8192, 1024, 2048, true, 2>;
 using MediumCfg = EngineCfg<512, 512, 16, 65536, 32768, 16384, false, 1>;
 #endif
 using GiantCfg = EngineCfg<512, 512, 1, 0, 0, 0, false, 1>;

@@ -19,8 +19,8 @@
 // A round:
 //   P1 materialize + classify every box (lane per box, queries mixed);
 //      group-wide atomicMin per query = first non-disjoint box j
-//   P2 atomicMin per query = first accepted box after j before the budget
-//      cut (the only box that can become the "drop" record)
+//      and atomicMin = first accepted box (if not j itself, the only
+//      candidate for the "drop" record, since boxes are in t_lo order)
 //   P3 one thread per query replays the reference's in-level events from
 //      (j, drop, cut) in O(1): normal return, budget return, queue
 //      exhaustion or continue (_kernel.py:176-324)
@@ -95,6 +95,98 @@ __device__ __forceinline__ unsigned long long group_excl_scan(unsigned long long
     return x - v;
   } else {
     return block_excl_scan<G>(v, sw, total);
+  }
+}
+
+// two exclusive sums over a group in one pass (shared barriers)
+template <int G>
+__device__ __forceinline__ void group_excl_scan2(unsigned long long v0, unsigned long long v1,
+                                                 unsigned long long* sw, unsigned long long& e0,
+                                                 unsigned long long& e1, unsigned long long& t0,
+                                                 unsigned long long& t1) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long x0 = v0, x1 = v1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y0 = __shfl_up_sync(0xffffffffu, x0, o);
+    const unsigned long long y1 = __shfl_up_sync(0xffffffffu, x1, o);
+    if (lane >= o) { x0 += y0; x1 += y1; }
+  }
+  if constexpr (G == 32) {
+    t0 = __shfl_sync(0xffffffffu, x0, 31);
+    t1 = __shfl_sync(0xffffffffu, x1, 31);
+    e0 = x0 - v0;
+    e1 = x1 - v1;
+  } else {
+    constexpr int NW = G / 32;
+    const int w = (threadIdx.x % G) >> 5;
+    if (lane == 31) { sw[w] = x0; sw[NW + w] = x1; }
+    __syncthreads();
+    if (w == 0) {
+      unsigned long long a0 = lane < NW ? sw[lane] : 0ull, a1 = lane < NW ? sw[NW + lane] : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y0 = __shfl_up_sync(0xffffffffu, a0, o);
+        const unsigned long long y1 = __shfl_up_sync(0xffffffffu, a1, o);
+        if (lane >= o) { a0 += y0; a1 += y1; }
+      }
+      if (lane < NW) { sw[lane] = a0; sw[NW + lane] = a1; }
+    }
+    __syncthreads();
+    e0 = (w ? sw[w - 1] : 0ull) + x0 - v0;
+    e1 = (w ? sw[NW + w - 1] : 0ull) + x1 - v1;
+    t0 = sw[NW - 1];
+    t1 = sw[2 * NW - 1];
+    __syncthreads();
+  }
+}
+
+// exclusive scans of ints over a group in one pass: forward max of vm, and
+// reverse min of vn (over the ranks above this one)
+template <int G>
+__device__ __forceinline__ void group_scan_maxfwd_minrev(int vm, int vn, int* swi, int& em,
+                                                         int& en) {
+  const int lane = threadIdx.x & 31;
+  int xm = vm, xn = vn;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int ym = __shfl_up_sync(0xffffffffu, xm, o);
+    const int yn = __shfl_down_sync(0xffffffffu, xn, o);
+    if (lane >= o) xm = max(xm, ym);
+    if (lane + o < 32) xn = min(xn, yn);
+  }
+  int exm = __shfl_up_sync(0xffffffffu, xm, 1);
+  int exn = __shfl_down_sync(0xffffffffu, xn, 1);
+  if (lane == 0) exm = -1;
+  if (lane == 31) exn = kIntMax;
+  if constexpr (G == 32) {
+    em = exm;
+    en = exn;
+  } else {
+    constexpr int NW = G / 32;
+    const int w = (threadIdx.x % G) >> 5;
+    if (lane == 31) swi[w] = xm;
+    if (lane == 0) swi[NW + w] = xn;
+    __syncthreads();
+    if (w == 0) {
+      int am = lane < NW ? swi[lane] : -1, an = lane < NW ? swi[NW + lane] : kIntMax;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ym = __shfl_up_sync(0xffffffffu, am, o);
+        const int yn = __shfl_down_sync(0xffffffffu, an, o);
+        if (lane >= o) am = max(am, ym);
+        if (lane + o < NW) an = min(an, yn);
+      }
+      int pm = __shfl_up_sync(0xffffffffu, am, 1);
+      int pn = __shfl_down_sync(0xffffffffu, an, 1);
+      if (lane == 0) pm = -1;
+      if (lane == NW - 1) pn = kIntMax;
+      if (lane < NW) { swi[2 * NW + lane] = pm; swi[3 * NW + lane] = pn; }
+    }
+    __syncthreads();
+    em = max(swi[2 * NW + w], exm);
+    en = min(swi[3 * NW + w], exn);
+    __syncthreads();
   }
 }
 
@@ -206,8 +298,8 @@ struct EngineShared {
   uint8_t unsorted[Q];
   uint8_t uniform[Q];    // dyadic t_max: every level has uniform widths (closed-form order)
   int segP0[Q];          // flat count of refining boxes before the segment
-  unsigned long long sw[Cfg::G / 32];
-  int swi[2 * (Cfg::G / 32)];
+  unsigned long long sw[2 * (Cfg::G / 32)];
+  int swi[4 * (Cfg::G / 32)];
   int any_general;
   int n_cur, n_next, admit_k, exhausted, A_tot, B_tot, rot;
   unsigned long long deferred;
@@ -460,21 +552,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       if ((f & 3) != kDisjoint) {
         wbc[i] = wb;
         atomicMin(&S.j[s], k);
+        // first accepted box: if it is not j itself it lies after j, and it is
+        // the only candidate for the drop record (boxes are in t_lo order)
+        if (f & 4) atomicMin(&S.acc[s], k);
       }
       fl[i] = f;
-    }
-    gsync<G>();
-    // ================= P2: first accepted box after j, before the cut
-    for (int i = tid; i < n; i += NT) {
-      const int s = sl[i];
-      if (s == kPNone) continue;
-      const int k = i - S.seg_off[s];
-      if (k <= S.j[s]) continue;
-      const long long cut = S.qp[s].max_checks - S.C[s] - 1;
-      const long long eend = S.seg_n[s] < cut ? S.seg_n[s] : cut;
-      if (k >= eend) continue;
-      const uint8_t f = fl[i];
-      if ((f & 3) != kDisjoint && (f & 4)) atomicMin(&S.acc[s], k);
     }
     gsync<G>();
     // ================= P3: per-query outcome (O(1) replay of the level's events)
@@ -568,15 +650,14 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         sP += 1;
       }
       if (general) S.any_general = 1;
-      unsigned long long tot;
-      const unsigned long long pre =
-          group_excl_scan<G>(((unsigned long long)sA << 32) | sB, S.sw, tot);
-      unsigned long long totP;
-      const int P0 = (int)group_excl_scan<G>((unsigned long long)sP, S.sw, totP);
-      const int carryM = group_scan_excl_int<G, false, true>(
-          lastHeadP >= 0 ? P0 + lastHeadP : -1, -1, S.swi);
-      carryN = group_scan_excl_int<G, true, false>(
-          firstHeadP >= 0 ? P0 + firstHeadP : kIntMax, kIntMax, S.swi);
+      unsigned long long pre, preP, tot, totP;
+      group_excl_scan2<G>(((unsigned long long)sA << 32) | sB, (unsigned long long)sP, S.sw, pre,
+                          preP, tot, totP);
+      const int P0 = (int)preP;
+      int carryM;
+      group_scan_maxfwd_minrev<G>(lastHeadP >= 0 ? P0 + lastHeadP : -1,
+                                  firstHeadP >= 0 ? P0 + firstHeadP : kIntMax, S.swi, carryM,
+                                  carryN);
       if (carryN == kIntMax) carryN = (int)totP;
       unsigned int Ar = (unsigned int)(pre >> 32), Br = (unsigned int)(pre & 0xffffffffu);
       int Pr = P0, M = carryM;
