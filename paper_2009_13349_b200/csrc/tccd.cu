@@ -40,6 +40,7 @@ struct Counters {
   unsigned long long evicted[3];  // evictions out of each tier (diagnostics)
   unsigned long long boxes[3];    // boxes handled per tier (diagnostics)
   unsigned long long pad[2];
+  unsigned long long phase[3][16];  // cycles per engine phase (TCCD_PHASE_PROF builds)
 };
 
 // A query that survived the root check, with its precomputed constants.
@@ -424,6 +425,7 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
     io.deferred = &a.ctr->deferred;
     io.evicted = &a.ctr->evicted[tier];
     io.boxes = &a.ctr->boxes[tier];
+    io.phase = a.ctr->phase[tier];
     if (tier == 0) { io.arenas = ws + L.light; io.arena_bytes = L.light_b; io.cap = LightCfg::CAP; }
     if (tier == 1) { io.arenas = ws + L.medium; io.arena_bytes = L.medium_b; io.cap = MediumCfg::CAP; }
     if (tier == 2) { io.arenas = ws + L.giant; io.arena_bytes = L.giant_b; io.cap = giant_cap(mcmax); }

@@ -336,6 +336,22 @@ __device__ __forceinline__ int split_dim(const Box& b, const double* kap, double
   return sdim;
 }
 
+#ifdef TCCD_PHASE_PROF
+// per-phase cycle accounting (diagnostic builds only)
+#define TCCD_PHASE(k)                                     \
+  do {                                                    \
+    if (tid == 0) {                                       \
+      const long long now_ = clock64();                   \
+      ph_acc[k] += (unsigned long long)(now_ - ph_last);  \
+      ph_last = now_;                                     \
+    }                                                     \
+  } while (0)
+#else
+#define TCCD_PHASE(k) \
+  do {                \
+  } while (0)
+#endif
+
 struct TierIO {
   const Pre* in;            // input queue
   unsigned long long* in_count;
@@ -349,6 +365,7 @@ struct TierIO {
   unsigned long long* deferred;
   unsigned long long* evicted;
   unsigned long long* boxes;
+  unsigned long long* phase;  // [16] cycles per phase (TCCD_PHASE_PROF builds)
 };
 
 template <class Cfg>
@@ -390,6 +407,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   int cur = 0;
   long long rounds = 0;
   unsigned long long evicted = 0, boxes = 0;
+#ifdef TCCD_PHASE_PROF
+  unsigned long long ph_acc[16] = {0};
+  long long ph_last = clock64();
+#endif
 
   auto evict = [&](int s) {
     const unsigned long long h = atomicAdd(io.out_count, 1ull);
@@ -451,6 +472,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       }
     }
     gsync<G>();
+    TCCD_PHASE(0);
     const int k_adm = S.admit_k;
     for (int s = tid; s < Q; s += NT) {
       if (S.qidx[s] < 0 && k_adm > 0) {
@@ -494,8 +516,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       S.unsorted[s] = 0;
     }
     gsync<G>();
+    TCCD_PHASE(1);
     if (tid == 0) { S.n_cur += k_adm; S.any_general = 0; }
     gsync<G>();
+    TCCD_PHASE(2);
     const int n = S.n_cur;
     if (n == 0) break;
     ++rounds;
@@ -559,6 +583,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       fl[i] = f;
     }
     gsync<G>();
+    TCCD_PHASE(3);
     // ================= P3: per-query outcome (O(1) replay of the level's events)
     for (int s = tid; s < Q; s += NT) {
       if (S.qidx[s] < 0) continue;
@@ -622,6 +647,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       if (done) S.qidx[s] = -1;
     }
     gsync<G>();
+    TCCD_PHASE(4);
     // ================= P4: child counts -> flat prefixes (A, B, refining boxes P)
     // Threads own contiguous chunks.  For uniform queries (dyadic t_max) the
     // next level's order is closed-form (see P4c); the run carries M (P at the
@@ -642,7 +668,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         if (f & kHead) { if (firstHeadP < 0) firstHeadP = sP; lastHeadP = sP; }
         if (!S.cont[s]) continue;
         general |= !S.uniform[s];
-        if (i - S.seg_off[s] < S.j[s]) continue;
+        // (boxes before j are disjoint, so they never refine)
         if ((f & 3) == kDisjoint || (f & 4)) continue;
         const int sdim = (f >> 3) & 3;
         sA += 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
@@ -671,7 +697,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         if (k == 0) { S.segA0[s] = (int)Ar; S.segB0[s] = (int)Br; S.segP0[s] = Pr; }
         offA[i] = S.uniform[s] ? (Off)M : (Off)Ar;  // uniform: run-start carry
         offB[i] = (Off)Br;
-        if (S.cont[s] && k >= S.j[s] && (f & 3) != kDisjoint && !(f & 4)) {
+        if (S.cont[s] && (f & 3) != kDisjoint && !(f & 4)) {
           const int sdim = (f >> 3) & 3;
           Ar += 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
           Br += sdim == 0 ? 1 : 0;
@@ -683,6 +709,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       A_end = (int)Ar;
     }
     gsync<G>();
+    TCCD_PHASE(5);
     // ================= P5: next-level layout (slot order), eviction, deferral
     // Levels above the tier's per-query cap go to the next tier.  Otherwise
     // the first K slots (rotating order) keep their children and the rest
@@ -698,9 +725,19 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       S.tot[s] = t;
     }
     gsync<G>();
+    TCCD_PHASE(6);
     if (tid < 32) {
       const int lane = tid;
-      constexpr int kPer = (Q + 31) / 32;
+      // layout order: all vertex-face queries, then all edge-edge queries
+      // (rotating start), so the next level's warps see one kind only and
+      // classify() does not diverge on the kind
+      constexpr int kV = 2 * Q;
+      constexpr int kPer = (kV + 31) / 32;
+      auto vslot = [&](int rpos) -> int {
+        if (rpos >= kV) return -1;
+        const int s = (S.rot + (rpos % Q)) % Q;
+        return S.qp[s].kind == (rpos >= Q ? 1 : 0) ? s : -1;
+      };
       int vt[kPer], vn[kPer];
       int st, sn, it, in, Nn, K;
       for (;;) {
@@ -708,8 +745,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
 #pragma unroll
         for (int m = 0; m < kPer; ++m) {
           const int rpos = lane * kPer + m;
-          const int s = (S.rot + rpos) % Q;
-          const bool ok = rpos < Q && S.cont[s] == 1;
+          const int s = vslot(rpos);
+          const bool ok = s >= 0 && S.cont[s] == 1;
           vt[m] = ok ? S.tot[s] : 0;
           vn[m] = ok ? S.seg_n[s] : 0;
           st += vt[m];
@@ -740,7 +777,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
 #pragma unroll
           for (int m = 0; m < kPer; ++m) {
             const int rpos = lane * kPer + m;
-            const int s = (S.rot + rpos) % Q;
+            const int s = vslot(rpos);
             if (vn[m] > 0) { evict(s); break; }
           }
         }
@@ -760,8 +797,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
 #pragma unroll
       for (int m = 0; m < kPer; ++m) {
         const int rpos = lane * kPer + m;
-        const int s = (S.rot + rpos) % Q;
-        if (rpos < Q && S.cont[s] == 1) {
+        const int s = vslot(rpos);
+        if (s >= 0 && S.cont[s] == 1) {
           if (rpos < K) {
             S.next_off[s] = ut;
           } else {
@@ -782,6 +819,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       }
     }
     gsync<G>();
+    TCCD_PHASE(7);
     // ================= P4c: next level of uniform queries, closed form; deferred carry
     // For dyadic t_max every box of a level has the same widths, hence the
     // same split dimension.  u/v split: the children are already in stable
@@ -809,7 +847,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           sln[pos] = (uint8_t)s;
           fln[pos] = f;
         }
-        if (cs != 0 && k >= S.j[s] && (f & 3) != kDisjoint && !(f & 4)) {
+        if (cs != 0 && (f & 3) != kDisjoint && !(f & 4)) {
           const int sdim = (f >> 3) & 3;
           Pr -= 1;
           Ar -= 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
@@ -844,6 +882,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       }
     }
     gsync<G>();
+    TCCD_PHASE(8);
     if (S.any_general) {
     // ================= P5b: A / B entries (key, push, ref); deferred carry-over
     for (int i = tid; i < n; i += NT) {
@@ -852,7 +891,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       const int k = i - S.seg_off[s];
       // entries are written for every query counted in P4 (kept, deferred or
       // evicted) so that no stale entry sits inside the flat A / B ranges
-      if (S.cont[s] == 0 || k < S.j[s]) continue;
+      if (S.cont[s] == 0) continue;
       const uint8_t f = fl[i];
       if ((f & 3) == kDisjoint || (f & 4)) continue;
       const int sdim = (f >> 3) & 3;
@@ -947,14 +986,19 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       }
     }
     gsync<G>();
+    TCCD_PHASE(9);
     if (tid == 0) S.n_cur = S.n_next;
     cur = nxt;
     gsync<G>();
+    TCCD_PHASE(10);
   }
   if (tid == 0) {
     atomicAdd(io.rounds, (unsigned long long)rounds);
     atomicAdd(io.deferred, S.deferred);
     atomicAdd(io.boxes, boxes);
+#ifdef TCCD_PHASE_PROF
+    for (int k = 0; k < 16; ++k) atomicAdd(&io.phase[k], ph_acc[k]);
+#endif
   }
   if (evicted) atomicAdd(io.evicted, evicted);
 }
