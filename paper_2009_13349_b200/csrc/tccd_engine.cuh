@@ -532,11 +532,24 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     uint8_t* const sl = slot_of[cur];
     uint8_t* const fl = flags[cur];
     // ================= P1: materialize + classify
+    // software pipeline: the reference of box i + 2*NT and the parent box of
+    // box i + NT are in flight while box i is classified
+    unsigned int r_cur = tid < n ? rf[tid] : kRefRoot;
+    Box p_cur;
+    if (!(r_cur & kRefRoot)) p_cur = bprev[r_cur & kRefSrcMask];
+    unsigned int r_nxt = tid + NT < n ? rf[tid + NT] : kRefRoot;
     for (int i = tid; i < n; i += NT) {
+      Box p_nxt;
+      if (!(r_nxt & kRefRoot)) p_nxt = bprev[r_nxt & kRefSrcMask];
+      const unsigned int r_nn = i + 2 * NT < n ? rf[i + 2 * NT] : kRefRoot;
+      const unsigned int r = r_cur;
+      const Box p = p_cur;
+      r_cur = r_nxt;
+      p_cur = p_nxt;
+      r_nxt = r_nn;
       const int s = sl[i];
       if (s == kPNone) continue;
       const QueryParams& qp = S.qp[s];
-      const unsigned int r = rf[i];
       Box b;
       uint8_t f = fl[i];  // head bit (+ class, for roots and deferred boxes)
       double wb = 0.0;
@@ -545,7 +558,6 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         wb = S.root_wb[s];
       } else {
         const int src = (int)(r & kRefSrcMask);
-        const Box p = bprev[src];
         if (r & kRefSelf) {
           b = p;
           if ((f & kClassified) && (f & 3) != kDisjoint) wb = wbp[src];
