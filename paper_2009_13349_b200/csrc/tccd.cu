@@ -39,7 +39,7 @@ struct Counters {
   unsigned long long deferred;    // level deferrals (diagnostics)
   unsigned long long evicted[3];  // evictions out of each tier (diagnostics)
   unsigned long long boxes[3];    // boxes handled per tier (diagnostics)
-  unsigned long long pad[2];
+  unsigned long long pool[3];     // handover pool fill (tiers 1, 2)
   unsigned long long phase[3][16];  // cycles per engine phase (TCCD_PHASE_PROF builds)
 };
 
@@ -51,6 +51,24 @@ struct Pre {
   double wb;           // root hull width (valid when flag says non-disjoint)
   unsigned int flag;   // root class flag (0: not classified yet)
   unsigned int pad;
+};
+
+struct Rec {  // first / drop record of a query (_kernel.py:158-171)
+  Box b;
+  double codom;
+  int level;
+  int pad;
+};
+
+// Handover state of a query evicted to the next tier with its next level
+// materialized (n > 0): the next tier resumes it instead of restarting.
+struct Hand {
+  long long C;       // checks done
+  long long off;     // first box of the level in the tier's handover pool
+  int level;         // BFS level of those boxes
+  int n;             // boxes (0: restart from the root)
+  Rec rec[2];        // first, drop
+  unsigned char have_first, have_drop, pad[6];
 };
 
 struct Args {
@@ -234,10 +252,10 @@ namespace tccd {
 
 //                   G    NT   Q   CAP    QCAP   ADMIT  SMEM   MINB
 #ifndef TCCD_LQ
-#define TCCD_LQ 64
+#define TCCD_LQ 32
 #endif
 #ifndef TCCD_LADMIT
-#define TCCD_LADMIT 2048
+#define TCCD_LADMIT 1024
 #endif
 #ifndef TCCD_LQCAP
 #define TCCD_LQCAP 1024
@@ -245,7 +263,17 @@ namespace tccd {
 #ifndef TCCD_MSMEM
 #define TCCD_MSMEM 1
 #endif
-using LightCfg = EngineCfg<256, 256, TCCD_LQ, 8192, TCCD_LQCAP, TCCD_LADMIT, true, 2>;
+#ifndef TCCD_LNT
+#define TCCD_LNT 128
+#endif
+#ifndef TCCD_LCAP
+#define TCCD_LCAP 4096
+#endif
+#ifndef TCCD_LMINB
+#define TCCD_LMINB 4
+#endif
+using LightCfg = EngineCfg<TCCD_LNT, TCCD_LNT, TCCD_LQ, TCCD_LCAP, TCCD_LQCAP, TCCD_LADMIT, true,
+                           TCCD_LMINB>;
 #if TCCD_MSMEM
 using MediumCfg = EngineCfg<512, 512, 16, 16384, 8192, 8192, true, 1>;
 #else
@@ -287,8 +315,10 @@ int device_sm_count(int hint) {
 
 long long giant_cap(long long mcmax) { return 2 * mcmax + 2; }
 
+constexpr long long kPool = 1LL << 24;  // handover pool boxes per tier transition
+
 struct Layout {
-  size_t ctr, queue[3], light, medium, giant, total;
+  size_t ctr, queue[3], hand[3], pbox[3], pflag[3], light, medium, giant, total;
   size_t light_b, medium_b, giant_b;
   int light_blocks, medium_blocks, giant_blocks;
 };
@@ -296,7 +326,7 @@ struct Layout {
 Layout layout(long long n, long long mcmax, int giant_blocks, int sms) {
   Layout L;
   const long long chunk = n < kChunk ? (n > 0 ? n : 1) : kChunk;
-  L.light_blocks = 2 * sms;
+  L.light_blocks = TCCD_LMINB * sms;
   L.medium_blocks = sms;
   L.giant_blocks = giant_blocks;
   L.light_b = align256(EngineArena<LightCfg>::bytes(LightCfg::CAP));
@@ -305,6 +335,12 @@ Layout layout(long long n, long long mcmax, int giant_blocks, int sms) {
   size_t o = 0;
   L.ctr = o; o += align256(sizeof(Counters));
   for (int k = 0; k < 3; ++k) { L.queue[k] = o; o += align256((size_t)chunk * sizeof(Pre)); }
+  L.hand[0] = L.pbox[0] = L.pflag[0] = 0;
+  for (int k = 1; k < 3; ++k) {
+    L.hand[k] = o; o += align256((size_t)chunk * sizeof(Hand));
+    L.pbox[k] = o; o += align256((size_t)kPool * sizeof(Box));
+    L.pflag[k] = o; o += align256((size_t)kPool);
+  }
   L.light = o; o += L.light_b * (size_t)L.light_blocks * groups_per_cta<LightCfg>();
   L.medium = o; o += L.medium_b * (size_t)L.medium_blocks * groups_per_cta<MediumCfg>();
   L.giant = o; o += L.giant_b * (size_t)L.giant_blocks;
@@ -417,6 +453,16 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
   auto io_for = [&](int tier) {
     TierIO io;
     io.in = queue[tier];
+    // (in heavy-only mode the prologue feeds the giant tier: no handovers)
+    io.in_hand = tier > 0 && !a.heavy_only ? (const Hand*)(ws + L.hand[tier]) : nullptr;
+    io.in_pbox = tier > 0 ? (const Box*)(ws + L.pbox[tier]) : nullptr;
+    io.in_pflag = tier > 0 ? (const uint8_t*)(ws + L.pflag[tier]) : nullptr;
+    io.in_maxsz = tier == 0 ? 1 : 2 * (tier == 1 ? LightCfg::QCAP : MediumCfg::QCAP);
+    io.out_hand = tier < 2 ? (Hand*)(ws + L.hand[tier + 1]) : nullptr;
+    io.out_pbox = tier < 2 ? (Box*)(ws + L.pbox[tier + 1]) : nullptr;
+    io.out_pflag = tier < 2 ? (uint8_t*)(ws + L.pflag[tier + 1]) : nullptr;
+    io.out_pool_count = tier < 2 ? &a.ctr->pool[tier + 1] : nullptr;
+    io.pool_cap = kPool;
     io.in_count = &a.ctr->q_count[tier];
     io.in_next = &a.ctr->q_next[tier];
     io.out = tier < 2 ? queue[tier + 1] : nullptr;

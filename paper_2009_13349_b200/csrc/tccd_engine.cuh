@@ -50,13 +50,8 @@ constexpr unsigned kRefSrcMask = (1u << 29) - 1;  // position in the previous bo
 constexpr unsigned kRefCb = 1u << 29;             // upper child
 constexpr unsigned kRefSelf = 1u << 30;           // the box itself (deferred level)
 constexpr unsigned kRefRoot = 1u << 31;           // the query's root box
+constexpr unsigned kRefExt = kRefRoot | kRefSelf;  // box src of the handover pool
 
-struct Rec {  // first / drop record of a slot
-  Box b;
-  double codom;
-  int level;
-  int pad;
-};
 
 template <int G_, int NT_, int Q_, int CAP_, int QCAP_, int ADMIT_, bool SMEM_, int MINB_>
 struct EngineCfg {
@@ -292,6 +287,9 @@ struct EngineShared {
   int segA0[Q], segB0[Q], segA1[Q], segB1[Q];
   int next_off[Q];
   int tot[Q];
+  long long hoff[Q];     // evicted with handover: pool offset of the level (-1: restart)
+  int adm_n[Q], adm_pos[Q], adm_slot[Q];
+  long long adm_off[Q];
   uint8_t root_flag[Q];
   uint8_t have_first[Q], have_drop[Q];
   uint8_t cont[Q];       // 1: children kept; 2: deferred; 3: evicted (children counted)
@@ -354,6 +352,15 @@ __device__ __forceinline__ int split_dim(const Box& b, const double* kap, double
 
 struct TierIO {
   const Pre* in;            // input queue
+  const Hand* in_hand;      // handover state of the input entries (nullptr: none)
+  const Box* in_pbox;       // handover pool the input levels live in
+  const uint8_t* in_pflag;
+  int in_maxsz;             // largest handed-over level
+  Hand* out_hand;           // handover state / pool of the next tier
+  Box* out_pbox;
+  uint8_t* out_pflag;
+  unsigned long long* out_pool_count;
+  long long pool_cap;
   unsigned long long* in_count;
   unsigned long long* in_next;
   Pre* out;                 // eviction queue of the next tier (nullptr: none)
@@ -412,13 +419,31 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   long long ph_last = clock64();
 #endif
 
-  auto evict = [&](int s) {
+  // Evict slot s (its next level has t boxes) to the next tier.  With room in
+  // the handover pool, the next level is materialized there (P4c / P6) and
+  // the next tier resumes the query; otherwise it restarts from the root.
+  auto evict = [&](int s, int t) {
     const unsigned long long h = atomicAdd(io.out_count, 1ull);
     Pre& p = io.out[h];
     p.q = S.qidx[s];
     for (int k = 0; k < 3; ++k) { p.eps[k] = S.qp[s].eps[k]; p.kap[k] = S.qp[s].kap[k]; }
     p.wb = 0.0;
     p.flag = 0;
+    long long off = -1;
+    if (io.out_hand) {
+      const unsigned long long o = atomicAdd(io.out_pool_count, (unsigned long long)t);
+      if ((long long)o + t <= io.pool_cap) off = (long long)o;
+      Hand& hd = io.out_hand[h];
+      hd.n = off >= 0 ? t : 0;
+      hd.off = off;
+      hd.C = S.C[s];
+      hd.level = S.level[s] + 1;
+      hd.rec[0] = S.rec[s][0];
+      hd.rec[1] = S.rec[s][1];
+      hd.have_first = S.have_first[s];
+      hd.have_drop = S.have_drop[s];
+    }
+    S.hoff[s] = off;
     S.qidx[s] = -1;
     S.cont[s] = 3;
     ++evicted;
@@ -457,6 +482,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         const unsigned long long groups = (unsigned long long)gridDim.x * (Cfg::NT / G);
         const long long share = (long long)((left + groups - 1) / groups);
         if (k > share) k = (int)(share > 0 ? share : 1);
+        if (io.in_maxsz > 1) {  // handed-over levels: keep room for the largest
+          int kk = room / io.in_maxsz;
+          if (kk < 1 && S.n_cur == 0) kk = 1;
+          if (k > kk) k = kk;
+        }
         long long base = 0;
         if (S.exhausted) k = 0;
         if (k > 0) {
@@ -474,6 +504,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     gsync<G>();
     TCCD_PHASE(0);
     const int k_adm = S.admit_k;
+    // step 1: one thread per admitted entry loads it into a free slot
     for (int s = tid; s < Q; s += NT) {
       if (S.qidx[s] < 0 && k_adm > 0) {
         const int w = s >> 5, lane = s & 31;
@@ -482,7 +513,6 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         if (r < k_adm) {
           const Pre& pre = io.in[S.admit_base + r];
           const long long q = pre.q;
-          const int pos = S.n_cur + r;
           double* P = S.P[s];
           const double* src = a.points + 24 * q;
 #pragma unroll
@@ -495,21 +525,67 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           load_params(a, q, qp);
           for (int k = 0; k < 3; ++k) { qp.eps[k] = pre.eps[k]; qp.kap[k] = pre.kap[k]; }
           S.qidx[s] = q;
-          S.C[s] = 0;
-          S.level[s] = 0;
-          S.have_first[s] = 0;
-          S.have_drop[s] = 0;
-          S.seg_off[s] = pos;
-          S.seg_n[s] = 1;
           S.root_flag[s] = (uint8_t)pre.flag;
           S.root_wb[s] = pre.wb;
           int ex;
           S.uniform[s] = frexp(qp.t_max, &ex) == 0.5;  // t_max a power of two
-          ar.ref[cur][pos] = kRefRoot;
-          slot_of[cur][pos] = (uint8_t)s;
-          flags[cur][pos] = (uint8_t)pre.flag | kHead;
+          int nr = 1;
+          long long off = -1;
+          if (io.in_hand && io.in_hand[S.admit_base + r].n > 0) {
+            // resume a query handed over by the previous tier
+            const Hand& hd = io.in_hand[S.admit_base + r];
+            nr = hd.n;
+            off = hd.off;
+            S.C[s] = hd.C;
+            S.level[s] = hd.level;
+            S.rec[s][0] = hd.rec[0];
+            S.rec[s][1] = hd.rec[1];
+            S.have_first[s] = hd.have_first;
+            S.have_drop[s] = hd.have_drop;
+          } else {
+            S.C[s] = 0;
+            S.level[s] = 0;
+            S.have_first[s] = 0;
+            S.have_drop[s] = 0;
+          }
+          S.adm_n[r] = nr;
+          S.adm_off[r] = off;
+          S.adm_slot[r] = s;
         }
       }
+    }
+    gsync<G>();
+    // step 2: segment offsets of the admitted levels
+    if (tid == 0) {
+      int pos = S.n_cur;
+      for (int r = 0; r < k_adm; ++r) {
+        S.adm_pos[r] = pos;
+        pos += S.adm_n[r];
+      }
+      S.n_next = pos;  // new fill (reused as scratch until P5)
+    }
+    gsync<G>();
+    // step 3: reference lists of the admitted levels
+    for (int r = 0; r < k_adm; ++r) {
+      const int s = S.adm_slot[r], pos = S.adm_pos[r], nr = S.adm_n[r];
+      const long long off = S.adm_off[r];
+      if (tid == 0) { S.seg_off[s] = pos; S.seg_n[s] = nr; }
+      if (off < 0) {
+        if (tid == 0) {
+          ar.ref[cur][pos] = kRefRoot;
+          slot_of[cur][pos] = (uint8_t)s;
+          flags[cur][pos] = S.root_flag[s] | kHead;
+        }
+      } else {
+        for (int b = tid; b < nr; b += NT) {
+          ar.ref[cur][pos + b] = kRefExt | (unsigned)(off + b);
+          slot_of[cur][pos + b] = (uint8_t)s;
+          flags[cur][pos + b] = io.in_pflag[off + b];
+        }
+      }
+    }
+    for (int s = tid; s < Q; s += NT) {
+      S.hoff[s] = -1;
       S.j[s] = kIntMax;
       S.acc[s] = kIntMax;
       S.cont[s] = 0;
@@ -517,7 +593,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     }
     gsync<G>();
     TCCD_PHASE(1);
-    if (tid == 0) { S.n_cur += k_adm; S.any_general = 0; }
+    if (tid == 0) { S.n_cur = k_adm > 0 ? S.n_next : S.n_cur; S.any_general = 0; }
     gsync<G>();
     TCCD_PHASE(2);
     const int n = S.n_cur;
@@ -534,13 +610,17 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     // ================= P1: materialize + classify
     // software pipeline: the reference of box i + 2*NT and the parent box of
     // box i + NT are in flight while box i is classified
+    // (handed-over boxes are read from the tier's handover pool)
+    const Box* const pool = io.in_pbox;
     unsigned int r_cur = tid < n ? rf[tid] : kRefRoot;
     Box p_cur;
     if (!(r_cur & kRefRoot)) p_cur = bprev[r_cur & kRefSrcMask];
+    else if ((r_cur & kRefExt) == kRefExt) p_cur = pool[r_cur & kRefSrcMask];
     unsigned int r_nxt = tid + NT < n ? rf[tid + NT] : kRefRoot;
     for (int i = tid; i < n; i += NT) {
       Box p_nxt;
       if (!(r_nxt & kRefRoot)) p_nxt = bprev[r_nxt & kRefSrcMask];
+      else if ((r_nxt & kRefExt) == kRefExt) p_nxt = pool[r_nxt & kRefSrcMask];
       const unsigned int r_nn = i + 2 * NT < n ? rf[i + 2 * NT] : kRefRoot;
       const unsigned int r = r_cur;
       const Box p = p_cur;
@@ -553,7 +633,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       Box b;
       uint8_t f = fl[i];  // head bit (+ class, for roots and deferred boxes)
       double wb = 0.0;
-      if (r & kRefRoot) {
+      if ((r & kRefExt) == kRefExt) {
+        b = p;  // handed over (unclassified)
+      } else if (r & kRefRoot) {
         b = Box{0.0, qp.t_max, 0.0, 1.0, 0.0, 1.0};
         wb = S.root_wb[s];
       } else {
@@ -732,7 +814,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       int t = 0;
       if (S.cont[s]) {
         t = (S.segA1[s] - S.segA0[s]) + (S.segB1[s] - S.segB0[s]);
-        if (t > qcap) evict(s);
+        if (t > qcap) evict(s, t);
       }
       S.tot[s] = t;
     }
@@ -790,7 +872,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           for (int m = 0; m < kPer; ++m) {
             const int rpos = lane * kPer + m;
             const int s = vslot(rpos);
-            if (vn[m] > 0) { evict(s); break; }
+            if (vn[m] > 0) { evict(s, S.tot[s]); break; }
           }
         }
         __syncwarp();
@@ -863,29 +945,43 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           const int sdim = (f >> 3) & 3;
           Pr -= 1;
           Ar -= 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
-          if (cs == 1 && S.uniform[s]) {
+          const bool hand = cs == 3 && S.hoff[s] >= 0;
+          if ((cs == 1 || hand) && S.uniform[s]) {
             const int M = (int)offA[i];
             const int S0 = S.segP0[s];
             const uint8_t hd = Pr == M ? kHead : 0;
-            const int base = S.next_off[s];
+            int rl, ru = -1;
             if (sdim == 0) {
-              const int rl = base + (M - S0) + (Pr - S0);
-              const int ru = base + (N - S0) + (Pr - S0);
-              outr[rl] = (unsigned)i;
-              sln[rl] = (uint8_t)s;
-              fln[rl] = hd;
-              outr[ru] = (unsigned)i | kRefCb;
-              sln[ru] = (uint8_t)s;
-              fln[ru] = hd;
+              rl = (M - S0) + (Pr - S0);
+              ru = (N - S0) + (Pr - S0);
             } else {
-              const int rl = base + (Ar - S.segA0[s]);
-              outr[rl] = (unsigned)i;
-              sln[rl] = (uint8_t)s;
-              fln[rl] = hd;
-              if (f & 32) {
-                outr[rl + 1] = (unsigned)i | kRefCb;
-                sln[rl + 1] = (uint8_t)s;
-                fln[rl + 1] = 0;
+              rl = Ar - S.segA0[s];
+              if (f & 32) ru = rl + 1;
+            }
+            const uint8_t hu = sdim == 0 ? hd : 0;
+            if (!hand) {
+              const int base = S.next_off[s];
+              outr[base + rl] = (unsigned)i;
+              sln[base + rl] = (uint8_t)s;
+              fln[base + rl] = hd;
+              if (ru >= 0) {
+                outr[base + ru] = (unsigned)i | kRefCb;
+                sln[base + ru] = (uint8_t)s;
+                fln[base + ru] = hu;
+              }
+            } else {
+              // materialize the handed-over level in the next tier's pool
+              const long long base = S.hoff[s];
+              const Box pb = bx[i];
+              double mid;
+              const int sd = split_dim(pb, S.qp[s].kap, mid);
+              Box c0, c1;
+              children(pb, sd, mid, c0, c1);
+              io.out_pbox[base + rl] = c0;
+              io.out_pflag[base + rl] = hd;
+              if (ru >= 0) {
+                io.out_pbox[base + ru] = c1;
+                io.out_pflag[base + ru] = hu;
               }
             }
           }
@@ -932,7 +1028,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       const int B_tot = S.B_tot;
       for (int b = tid + 1; b < B_tot; b += NT) {
         const int s = sl[ar.bref[b] & kRefSrcMask];
-        if (S.cont[s] != 1 || S.uniform[s] || b <= S.segB0[s]) continue;
+        if (!(S.cont[s] == 1 || (S.cont[s] == 3 && S.hoff[s] >= 0)) || S.uniform[s] ||
+            b <= S.segB0[s])
+          continue;
         if (ar.bkey[b - 1] > ar.bkey[b]) S.unsorted[s] = 1;
       }
     }
@@ -948,7 +1046,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         const int x = isA ? e : e - A_tot;
         const unsigned int r = isA ? ar.aref[x] : ar.bref[x];
         const int s = sl[r & kRefSrcMask];
-        if (S.cont[s] != 1 || S.uniform[s]) continue;
+        const bool hand = S.cont[s] == 3 && S.hoff[s] >= 0;
+        if (!(S.cont[s] == 1 || hand) || S.uniform[s]) continue;
         const unsigned long long kk = isA ? ar.akey[x] : ar.bkey[x];
         const unsigned int pp = isA ? ar.apush[x] : ar.bpush[x];
         int rank;
@@ -978,10 +1077,20 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           for (int m = S.segB0[s]; m < S.segB1[s]; ++m)
             rank += kp_less(ar.bkey[m], ar.bpush[m], kk, pp) ? 1 : 0;
         }
-        const int pos = S.next_off[s] + rank;
-        out[pos] = r;
-        sln[pos] = (uint8_t)s;
-        fln[pos] = 0;
+        if (!hand) {
+          const int pos = S.next_off[s] + rank;
+          out[pos] = r;
+          sln[pos] = (uint8_t)s;
+          fln[pos] = 0;
+        } else {
+          const Box pb = bx[r & kRefSrcMask];
+          double mid;
+          const int sd = split_dim(pb, S.qp[s].kap, mid);
+          Box c0, c1;
+          children(pb, sd, mid, c0, c1);
+          io.out_pbox[S.hoff[s] + rank] = (r & kRefCb) ? c1 : c0;
+          io.out_pflag[S.hoff[s] + rank] = 0;
+        }
       }
     }
     gsync<G>();

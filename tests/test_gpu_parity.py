@@ -72,6 +72,11 @@ def _vs_oracle(w, cuda, sep=None, t_max=None, heavy_only=False):
     (4, 20_000, 30_000, dict(sep=1e-8)),
     (4, 60_000, 300, dict(sep=1e-5)),
     (4, 61_000, 40, dict(sep=1e-3)),
+    # non-dyadic t_max on queries whose levels outgrow the light / medium
+    # tiers: the general ordering path plus tier handover
+    (1, 40_000, 20_000, dict(t_max=0.6)),
+    (2, 9_000, 2_000, dict(t_max=0.7)),
+    (4, 62_000, 100, dict(sep=1e-5, t_max=0.9)),
 ])
 def test_workload_samples_vs_oracle(cuda, config, start, count, kw):
     from paper_2009_13349_b200 import workloads as W
