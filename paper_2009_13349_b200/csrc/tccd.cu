@@ -267,10 +267,10 @@ namespace tccd {
 #define TCCD_LNT 128
 #endif
 #ifndef TCCD_LCAP
-#define TCCD_LCAP 4096
+#define TCCD_LCAP 3072
 #endif
 #ifndef TCCD_LMINB
-#define TCCD_LMINB 4
+#define TCCD_LMINB 5
 #endif
 using LightCfg = EngineCfg<TCCD_LNT, TCCD_LNT, TCCD_LQ, TCCD_LCAP, TCCD_LQCAP, TCCD_LADMIT, true,
                            TCCD_LMINB>;

@@ -301,6 +301,7 @@ struct EngineShared {
   int any_general;
   int n_cur, n_next, admit_k, exhausted, A_tot, B_tot, rot;
   unsigned long long deferred;
+  int deferred_last;     // queries deferred in the previous round
   long long admit_base;
   unsigned int free_mask[(Q + 31) / 32];
 };
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   const unsigned long long in_total = *(volatile unsigned long long*)io.in_count;
   const int tid = threadIdx.x % G;  // rank within the group
   for (int s = tid; s < Q; s += NT) S.qidx[s] = -1;
-  if (tid == 0) { S.n_cur = 0; S.exhausted = 0; S.rot = 0; S.deferred = 0; }
+  if (tid == 0) { S.n_cur = 0; S.exhausted = 0; S.rot = 0; S.deferred = 0; S.deferred_last = 0; }
   gsync<G>();
   int cur = 0;
   long long rounds = 0;
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         }
         long long base = 0;
         if (S.exhausted) k = 0;
+        if (S.deferred_last) k = 0;  // deferred queries get the room first (no starvation)
         if (k > 0) {
           base = (long long)atomicAdd(io.in_next, (unsigned long long)k);
           if ((unsigned long long)base >= in_total) { k = 0; S.exhausted = 1; }
@@ -910,6 +912,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         S.n_next = cT + (Nn - cN);
         S.rot = (S.rot + 1) % Q;
         S.deferred += deferred;
+        S.deferred_last = deferred;
       }
     }
     gsync<G>();

@@ -28,7 +28,7 @@ for rep in range(2):
     torch.cuda.synchronize()
 ws = solver._workspaces[("cuda", 0)]
 ctr = ws[:512].cpu().view(torch.int64)
-ph = ctr[16:16 + 48].view(3, 16)
+ph = ctr[17:17 + 48].view(3, 16)  # Counters: 17 u64 before phase[3][16]
 for t, name in enumerate(["light", "medium", "giant"]):
     tot = int(ph[t].sum())
     if not tot:
