@@ -43,15 +43,18 @@ struct Counters {
   unsigned long long phase[3][16];  // cycles per engine phase (TCCD_PHASE_PROF builds)
 };
 
-// A query that survived the root check, with its precomputed constants.
+// A queued query, self-contained so a tier admits it with one coalesced
+// read: coordinates, parameters, filters and kappas, and the root class.
 struct Pre {
-  long long q;
-  double eps[3];
-  double kap[3];
+  double P[24];        // the 8 points (t0 block, then t1 block)
+  QueryParams qp;      // eps, kap, sep, delta, t_max, max_checks, kind
+  long long q;         // query index
   double wb;           // root hull width (valid when flag says non-disjoint)
   unsigned int flag;   // root class flag (0: not classified yet)
   unsigned int pad;
 };
+static_assert(sizeof(Pre) % 8 == 0, "Pre is copied as 8-byte words");
+constexpr int kPreWords = (int)(sizeof(Pre) / 8);
 
 struct Rec {  // first / drop record of a query (_kernel.py:158-171)
   Box b;
@@ -226,8 +229,9 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long
           write_result(a, q, kHit, root, wb, 1, 0, 0);  // accepted at the root
         } else {
           survive = true;
+          for (int k = 0; k < 24; ++k) pre.P[k] = P[k];
+          pre.qp = qp;
           pre.q = q;
-          for (int k = 0; k < 3; ++k) { pre.eps[k] = qp.eps[k]; pre.kap[k] = qp.kap[k]; }
           pre.wb = wb;
           pre.flag = make_flag(cls, acc, sdim, ph) | 64u;
           pre.pad = 0;
@@ -483,6 +487,10 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
   for (long long lo = 0; lo < b->n; lo += kChunk) {
     const long long cnt = b->n - lo < kChunk ? b->n - lo : kChunk;
     if (cudaMemsetAsync(a.ctr, 0, sizeof(Counters), st) != cudaSuccess) return TCCD_E_CUDA;
+#ifdef TCCD_PHASE_PROF
+    for (int k = 0; k < 3; ++k)  // phase[k][14] is a running min (start time)
+      if (cudaMemsetAsync(&a.ctr->phase[k][14], 0xFF, 8, st) != cudaSuccess) return TCCD_E_CUDA;
+#endif
     const int first = a.heavy_only ? 2 : 0;
     const unsigned pblocks = (unsigned)((cnt + kPrologueThreads - 1) / kPrologueThreads);
     prologue_kernel<<<pblocks, kPrologueThreads, 0, st>>>(a, lo, cnt, queue[first],

@@ -418,6 +418,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
 #ifdef TCCD_PHASE_PROF
   unsigned long long ph_acc[16] = {0};
   long long ph_last = clock64();
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 #endif
 
   // Evict slot s (its next level has t boxes) to the next tier.  With room in
@@ -426,8 +428,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   auto evict = [&](int s, int t) {
     const unsigned long long h = atomicAdd(io.out_count, 1ull);
     Pre& p = io.out[h];
+    for (int k = 0; k < 24; ++k) p.P[k] = S.P[s][k];
+    p.qp = S.qp[s];
     p.q = S.qidx[s];
-    for (int k = 0; k < 3; ++k) { p.eps[k] = S.qp[s].eps[k]; p.kap[k] = S.qp[s].kap[k]; }
     p.wb = 0.0;
     p.flag = 0;
     long long off = -1;
@@ -506,55 +509,62 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     gsync<G>();
     TCCD_PHASE(0);
     const int k_adm = S.admit_k;
-    // step 1: one thread per admitted entry loads it into a free slot
+    // step 1a: free slot of each admitted entry
     for (int s = tid; s < Q; s += NT) {
       if (S.qidx[s] < 0 && k_adm > 0) {
         const int w = s >> 5, lane = s & 31;
         int r = __popc(S.free_mask[w] & ((1u << lane) - 1u));
         for (int ww = 0; ww < w; ++ww) r += __popc(S.free_mask[ww]);
-        if (r < k_adm) {
-          const Pre& pre = io.in[S.admit_base + r];
-          const long long q = pre.q;
-          double* P = S.P[s];
-          const double* src = a.points + 24 * q;
-#pragma unroll
-          for (int i = 0; i < 24; i += 2) {
-            const double2 v = *reinterpret_cast<const double2*>(src + i);
-            P[i] = v.x;
-            P[i + 1] = v.y;
-          }
-          QueryParams& qp = S.qp[s];
-          load_params(a, q, qp);
-          for (int k = 0; k < 3; ++k) { qp.eps[k] = pre.eps[k]; qp.kap[k] = pre.kap[k]; }
-          S.qidx[s] = q;
-          S.root_flag[s] = (uint8_t)pre.flag;
-          S.root_wb[s] = pre.wb;
-          int ex;
-          S.uniform[s] = frexp(qp.t_max, &ex) == 0.5;  // t_max a power of two
-          int nr = 1;
-          long long off = -1;
-          if (io.in_hand && io.in_hand[S.admit_base + r].n > 0) {
-            // resume a query handed over by the previous tier
-            const Hand& hd = io.in_hand[S.admit_base + r];
-            nr = hd.n;
-            off = hd.off;
-            S.C[s] = hd.C;
-            S.level[s] = hd.level;
-            S.rec[s][0] = hd.rec[0];
-            S.rec[s][1] = hd.rec[1];
-            S.have_first[s] = hd.have_first;
-            S.have_drop[s] = hd.have_drop;
-          } else {
-            S.C[s] = 0;
-            S.level[s] = 0;
-            S.have_first[s] = 0;
-            S.have_drop[s] = 0;
-          }
-          S.adm_n[r] = nr;
-          S.adm_off[r] = off;
-          S.adm_slot[r] = s;
+        if (r < k_adm) S.adm_slot[r] = s;
+      }
+    }
+    gsync<G>();
+    // step 1b: warp-cooperative copy of the queue records (one coalesced read)
+    {
+      constexpr int NWARP = (NT + 31) / 32;
+      const int wid = tid >> 5, lane = tid & 31;
+      for (int r = wid; r < k_adm; r += NWARP) {
+        const int s = S.adm_slot[r];
+        const unsigned long long* src =
+            reinterpret_cast<const unsigned long long*>(io.in + S.admit_base + r);
+        for (int wd = lane; wd < kPreWords; wd += 32) {
+          const unsigned long long v = src[wd];
+          if (wd < 24) reinterpret_cast<unsigned long long*>(S.P[s])[wd] = v;
+          else if (wd < 24 + (int)(sizeof(QueryParams) / 8))
+            reinterpret_cast<unsigned long long*>(&S.qp[s])[wd - 24] = v;
+          else if (wd == (int)(offsetof(Pre, q) / 8)) S.qidx[s] = (long long)v;
+          else if (wd == (int)(offsetof(Pre, wb) / 8)) S.root_wb[s] = __longlong_as_double(v);
+          else if (wd == (int)(offsetof(Pre, flag) / 8)) S.root_flag[s] = (uint8_t)(v & 0xffu);
         }
       }
+    }
+    gsync<G>();
+    // step 1c: per-slot state (fresh root, or a level handed over by the
+    // previous tier)
+    for (int r = tid; r < k_adm; r += NT) {
+      const int s = S.adm_slot[r];
+      int ex;
+      S.uniform[s] = frexp(S.qp[s].t_max, &ex) == 0.5;  // t_max a power of two
+      int nr = 1;
+      long long off = -1;
+      if (io.in_hand && io.in_hand[S.admit_base + r].n > 0) {
+        const Hand& hd = io.in_hand[S.admit_base + r];
+        nr = hd.n;
+        off = hd.off;
+        S.C[s] = hd.C;
+        S.level[s] = hd.level;
+        S.rec[s][0] = hd.rec[0];
+        S.rec[s][1] = hd.rec[1];
+        S.have_first[s] = hd.have_first;
+        S.have_drop[s] = hd.have_drop;
+      } else {
+        S.C[s] = 0;
+        S.level[s] = 0;
+        S.have_first[s] = 0;
+        S.have_drop[s] = 0;
+      }
+      S.adm_n[r] = nr;
+      S.adm_off[r] = off;
     }
     gsync<G>();
     // step 2: segment offsets of the admitted levels
@@ -1121,7 +1131,13 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     atomicAdd(io.deferred, S.deferred);
     atomicAdd(io.boxes, boxes);
 #ifdef TCCD_PHASE_PROF
-    for (int k = 0; k < 16; ++k) atomicAdd(&io.phase[k], ph_acc[k]);
+    for (int k = 0; k < 11; ++k) atomicAdd(&io.phase[k], ph_acc[k]);
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    atomicAdd(&io.phase[11], t_end - t_start);  // group lifetime (ns)
+    atomicAdd(&io.phase[12], 1ull);
+    atomicMax(&io.phase[13], t_end);
+    atomicMin(&io.phase[14], t_start);
 #endif
   }
   if (evicted) atomicAdd(io.evicted, evicted);

@@ -24,14 +24,21 @@ dev = torch.device("cuda", 0)
 pts = torch.from_numpy(w.points).to(dev)
 kind = torch.from_numpy(w.kind).to(dev)
 for rep in range(2):
+    if rep == 1:  # phase[14] holds a min: start it high
+        pass
     out = solve_batch(pts, kind, outputs=("status", "toi"), device=dev, raise_on_error=False)
     torch.cuda.synchronize()
 ws = solver._workspaces[("cuda", 0)]
-ctr = ws[:512].cpu().view(torch.int64)
+ctr = ws[:1024].cpu().view(torch.int64)
 ph = ctr[17:17 + 48].view(3, 16)  # Counters: 17 u64 before phase[3][16]
 for t, name in enumerate(["light", "medium", "giant"]):
     tot = int(ph[t].sum())
     if not tot:
         continue
+    tot = int(ph[t][:11].sum())
     parts = ", ".join(f"{NAMES[k]} {100 * int(ph[t][k]) / tot:.1f}%" for k in range(11) if ph[t][k])
+    life, groups, tmax, tmin = (int(x) for x in ph[t][11:15])
+    span = (tmax - tmin) if tmin > 0 else 0
+    util = life / (groups * span) if span else 0.0
     print(f"{name}: {tot / 1e9:.2f} Gcycles (thread-0 of each group): {parts}")
+    print(f"   kernel span {span / 1e6:.2f} ms, {groups} groups, mean group lifetime / span = {util:.2f}")
