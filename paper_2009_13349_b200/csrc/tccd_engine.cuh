@@ -767,13 +767,18 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       unsigned int sA = 0, sB = 0;
       int sP = 0, lastHeadP = -1, firstHeadP = -1;
       bool general = false;
+      // (segments are contiguous: per-query values are cached while a
+      // chunk stays inside one segment)
+      int cs = -1;
+      bool c_cont = false, c_uni = false;
       for (int i = lo4; i < hi4; ++i) {
         const int s = sl[i];
         if (s == kPNone) continue;
+        if (s != cs) { cs = s; c_cont = S.cont[s] != 0; c_uni = S.uniform[s] != 0; }
         const uint8_t f = fl[i];
         if (f & kHead) { if (firstHeadP < 0) firstHeadP = sP; lastHeadP = sP; }
-        if (!S.cont[s]) continue;
-        general |= !S.uniform[s];
+        if (!c_cont) continue;
+        general |= !c_uni;
         // (boxes before j are disjoint, so they never refine)
         if ((f & 3) == kDisjoint || (f & 4)) continue;
         const int sdim = (f >> 3) & 3;
@@ -794,22 +799,30 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       unsigned int Ar = (unsigned int)(pre >> 32), Br = (unsigned int)(pre & 0xffffffffu);
       int Pr = P0, M = carryM;
       if (tid == 0) { S.A_tot = (int)(tot >> 32); S.B_tot = (int)(tot & 0xffffffffu); }
+      cs = -1;
+      int c_off = 0, c_last = 0;
       for (int i = lo4; i < hi4; ++i) {
         const int s = sl[i];
         if (s == kPNone) continue;
-        const int k = i - S.seg_off[s];
+        if (s != cs) {
+          cs = s;
+          c_off = S.seg_off[s];
+          c_last = c_off + S.seg_n[s] - 1;
+          c_cont = S.cont[s] != 0;
+          c_uni = S.uniform[s] != 0;
+        }
         const uint8_t f = fl[i];
         if (f & kHead) M = Pr;
-        if (k == 0) { S.segA0[s] = (int)Ar; S.segB0[s] = (int)Br; S.segP0[s] = Pr; }
-        offA[i] = S.uniform[s] ? (Off)M : (Off)Ar;  // uniform: run-start carry
+        if (i == c_off) { S.segA0[s] = (int)Ar; S.segB0[s] = (int)Br; S.segP0[s] = Pr; }
+        offA[i] = c_uni ? (Off)M : (Off)Ar;  // uniform: run-start carry
         offB[i] = (Off)Br;
-        if (S.cont[s] && (f & 3) != kDisjoint && !(f & 4)) {
+        if (c_cont && (f & 3) != kDisjoint && !(f & 4)) {
           const int sdim = (f >> 3) & 3;
           Ar += 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
           Br += sdim == 0 ? 1 : 0;
           Pr += 1;
         }
-        if (k == S.seg_n[s] - 1) { S.segA1[s] = (int)Ar; S.segB1[s] = (int)Br; }
+        if (i == c_last) { S.segA1[s] = (int)Ar; S.segB1[s] = (int)Br; }
       }
       P_end = Pr;
       A_end = (int)Ar;
@@ -942,14 +955,25 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       unsigned int* const outr = ar.ref[nxt];
       uint8_t* const sln = slot_of[nxt];
       uint8_t* const fln = flags[nxt];
+      int cslot = -1, cs = 0, c_off = 0, c_next = 0, c_S0 = 0, c_A0 = 0;
+      bool c_uni = false, c_hand = false;
       for (int i = hi4 - 1; i >= lo4; --i) {
         const int s = sl[i];
         if (s == kPNone) continue;
+        if (s != cslot) {
+          cslot = s;
+          cs = S.cont[s];
+          c_off = S.seg_off[s];
+          c_next = S.next_off[s];
+          c_S0 = S.segP0[s];
+          c_A0 = S.segA0[s];
+          c_uni = S.uniform[s] != 0;
+          c_hand = cs == 3 && S.hoff[s] >= 0;
+        }
         const uint8_t f = fl[i];
-        const int k = i - S.seg_off[s];
-        const int cs = S.cont[s];
+        const int k = i - c_off;
         if (cs == 2) {
-          const int pos = S.next_off[s] + k;
+          const int pos = c_next + k;
           outr[pos] = (unsigned)i | kRefSelf;
           sln[pos] = (uint8_t)s;
           fln[pos] = f;
@@ -958,22 +982,22 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           const int sdim = (f >> 3) & 3;
           Pr -= 1;
           Ar -= 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
-          const bool hand = cs == 3 && S.hoff[s] >= 0;
-          if ((cs == 1 || hand) && S.uniform[s]) {
+          const bool hand = c_hand;
+          if ((cs == 1 || hand) && c_uni) {
             const int M = (int)offA[i];
-            const int S0 = S.segP0[s];
+            const int S0 = c_S0;
             const uint8_t hd = Pr == M ? kHead : 0;
             int rl, ru = -1;
             if (sdim == 0) {
               rl = (M - S0) + (Pr - S0);
               ru = (N - S0) + (Pr - S0);
             } else {
-              rl = Ar - S.segA0[s];
+              rl = Ar - c_A0;
               if (f & 32) ru = rl + 1;
             }
             const uint8_t hu = sdim == 0 ? hd : 0;
             if (!hand) {
-              const int base = S.next_off[s];
+              const int base = c_next;
               outr[base + rl] = (unsigned)i;
               sln[base + rl] = (uint8_t)s;
               fln[base + rl] = hd;
