@@ -93,6 +93,31 @@ __device__ __forceinline__ unsigned long long group_excl_scan(unsigned long long
   }
 }
 
+// Byte reads from a 16-byte-aligned array through a one-vector cache: a
+// thread walking a contiguous chunk issues one 16-byte load per 16 boxes
+// (used where the per-box bookkeeping lives in global memory).
+template <bool VEC>
+struct ByteVecReader {
+  const uint8_t* p;
+  int base;
+  uint4 v;
+  __device__ __forceinline__ explicit ByteVecReader(const uint8_t* q) : p(q), base(-1) {}
+  __device__ __forceinline__ uint8_t operator()(int i) {
+    if constexpr (!VEC) {
+      return p[i];
+    } else {
+      const int b = i & ~15;
+      if (b != base) {
+        base = b;
+        v = *reinterpret_cast<const uint4*>(p + b);
+      }
+      const int k = (i >> 2) & 3;
+      const unsigned w = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+      return (uint8_t)(w >> ((i & 3) * 8));
+    }
+  }
+};
+
 // two exclusive sums over a group in one pass (shared barriers)
 template <int G>
 __device__ __forceinline__ void group_excl_scan2(unsigned long long v0, unsigned long long v1,
@@ -759,8 +784,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     // next level's order is closed-form (see P4c); the run carries M (P at the
     // head of the current run) and N (P at the next head) come from a
     // forward max-scan and a reverse min-scan over the chunks.
-    const int c4 = (n + NT - 1) / NT;
-    const int lo4 = tid * c4;
+    // (global-memory bookkeeping: 16-box aligned chunks for vector loads)
+    const int c4 = Cfg::SMEM ? (n + NT - 1) / NT : (((n + NT - 1) / NT + 15) & ~15);
+    const int lo4 = tid * c4 < n ? tid * c4 : n;
     const int hi4 = lo4 + c4 < n ? lo4 + c4 : n;
     int P_end, A_end, carryN;
     {
@@ -771,11 +797,12 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       // chunk stays inside one segment)
       int cs = -1;
       bool c_cont = false, c_uni = false;
+      ByteVecReader<!Cfg::SMEM> rsl(sl), rfl(fl);
       for (int i = lo4; i < hi4; ++i) {
-        const int s = sl[i];
+        const int s = rsl(i);
         if (s == kPNone) continue;
         if (s != cs) { cs = s; c_cont = S.cont[s] != 0; c_uni = S.uniform[s] != 0; }
-        const uint8_t f = fl[i];
+        const uint8_t f = rfl(i);
         if (f & kHead) { if (firstHeadP < 0) firstHeadP = sP; lastHeadP = sP; }
         if (!c_cont) continue;
         general |= !c_uni;
@@ -799,10 +826,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       unsigned int Ar = (unsigned int)(pre >> 32), Br = (unsigned int)(pre & 0xffffffffu);
       int Pr = P0, M = carryM;
       if (tid == 0) { S.A_tot = (int)(tot >> 32); S.B_tot = (int)(tot & 0xffffffffu); }
+      ByteVecReader<!Cfg::SMEM> rsl2(sl), rfl2(fl);
       cs = -1;
       int c_off = 0, c_last = 0;
       for (int i = lo4; i < hi4; ++i) {
-        const int s = sl[i];
+        const int s = rsl2(i);
         if (s == kPNone) continue;
         if (s != cs) {
           cs = s;
@@ -811,7 +839,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           c_cont = S.cont[s] != 0;
           c_uni = S.uniform[s] != 0;
         }
-        const uint8_t f = fl[i];
+        const uint8_t f = rfl2(i);
         if (f & kHead) M = Pr;
         if (i == c_off) { S.segA0[s] = (int)Ar; S.segB0[s] = (int)Br; S.segP0[s] = Pr; }
         offA[i] = c_uni ? (Off)M : (Off)Ar;  // uniform: run-start carry
@@ -955,10 +983,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       unsigned int* const outr = ar.ref[nxt];
       uint8_t* const sln = slot_of[nxt];
       uint8_t* const fln = flags[nxt];
+      ByteVecReader<!Cfg::SMEM> rsl(sl), rfl(fl);
       int cslot = -1, cs = 0, c_off = 0, c_next = 0, c_S0 = 0, c_A0 = 0;
       bool c_uni = false, c_hand = false;
       for (int i = hi4 - 1; i >= lo4; --i) {
-        const int s = sl[i];
+        const int s = rsl(i);
         if (s == kPNone) continue;
         if (s != cslot) {
           cslot = s;
@@ -970,7 +999,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           c_uni = S.uniform[s] != 0;
           c_hand = cs == 3 && S.hoff[s] >= 0;
         }
-        const uint8_t f = fl[i];
+        const uint8_t f = rfl(i);
         const int k = i - c_off;
         if (cs == 2) {
           const int pos = c_next + k;
