@@ -106,7 +106,7 @@ struct ByteVecReader {
     if constexpr (!VEC) {
       return p[i];
     } else {
-      const int b = i & ~15;
+      const int b = i & ~15;  // (16-byte aligned chunk of bytes)
       if (b != base) {
         base = b;
         v = *reinterpret_cast<const uint4*>(p + b);
@@ -114,6 +114,35 @@ struct ByteVecReader {
       const int k = (i >> 2) & 3;
       const unsigned w = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
       return (uint8_t)(w >> ((i & 3) * 8));
+    }
+  }
+};
+
+// same for 16-bit / 32-bit offsets (a 16-byte vector holds 8 / 4 of them)
+template <bool VEC, typename T>
+struct OffVecReader {
+  static constexpr int PER = 16 / (int)sizeof(T);
+  const T* p;
+  int base;
+  uint4 v;
+  __device__ __forceinline__ explicit OffVecReader(const T* q) : p(q), base(-1) {}
+  __device__ __forceinline__ int operator()(int i) {
+    if constexpr (!VEC) {
+      return (int)p[i];
+    } else {
+      const int b = i & ~(PER - 1);
+      if (b != base) {
+        base = b;
+        v = *reinterpret_cast<const uint4*>(p + b);
+      }
+      const int e = i & (PER - 1);
+      if constexpr (sizeof(T) == 4) {
+        return (int)(e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w)));
+      } else {
+        const int k = e >> 1;
+        const unsigned w = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+        return (int)((w >> ((e & 1) * 16)) & 0xffffu);
+      }
     }
   }
 };
@@ -984,6 +1013,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       uint8_t* const sln = slot_of[nxt];
       uint8_t* const fln = flags[nxt];
       ByteVecReader<!Cfg::SMEM> rsl(sl), rfl(fl);
+      OffVecReader<!Cfg::SMEM, Off> roffA(offA);
       int cslot = -1, cs = 0, c_off = 0, c_next = 0, c_S0 = 0, c_A0 = 0;
       bool c_uni = false, c_hand = false;
       for (int i = hi4 - 1; i >= lo4; --i) {
@@ -1013,7 +1043,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           Ar -= 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
           const bool hand = c_hand;
           if ((cs == 1 || hand) && c_uni) {
-            const int M = (int)offA[i];
+            const int M = roffA(i);
             const int S0 = c_S0;
             const uint8_t hd = Pr == M ? kHead : 0;
             int rl, ru = -1;
