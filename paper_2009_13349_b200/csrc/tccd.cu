@@ -211,12 +211,13 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long
       st = filters(P, qp.kind, qp.sep, qp.eps);
     }
     const Box root = {0.0, qp.t_max, 0.0, 1.0, 0.0, 1.0};
+    qp.tame = tame_coords(P);
     if (st != kHit) {
       write_result(a, q, st, root, 0.0, 0, 0, 0);
     } else {
       kappas(P, qp.kind, qp.t_max, qp.kap);
       double wb;
-      const int cls = classify(P, qp.kind, root, qp.eps, qp.sep, wb);
+      const int cls = classify(P, qp.kind, root, qp.eps, qp.sep, wb, qp.tame != 0);
       if (cls == kDisjoint) {
         // the queue empties after one check (_kernel.py:188-199, 321-324)
         write_result(a, q, kFree, root, 0.0, 1, 0, 0);
@@ -278,8 +279,24 @@ namespace tccd {
 #endif
 using LightCfg = EngineCfg<TCCD_LNT, TCCD_LNT, TCCD_LQ, TCCD_LCAP, TCCD_LQCAP, TCCD_LADMIT, true,
                            TCCD_LMINB>;
+#ifndef TCCD_MNT
+#define TCCD_MNT 512
+#endif
+#ifndef TCCD_MQ
+#define TCCD_MQ 16
+#endif
+#ifndef TCCD_MCAP
+#define TCCD_MCAP 16384
+#endif
+#ifndef TCCD_MADMIT
+#define TCCD_MADMIT 8192
+#endif
+#ifndef TCCD_MMINB
+#define TCCD_MMINB 1
+#endif
 #if TCCD_MSMEM
-using MediumCfg = EngineCfg<512, 512, 16, 16384, 8192, 8192, true, 1>;
+using MediumCfg = EngineCfg<TCCD_MNT, TCCD_MNT, TCCD_MQ, TCCD_MCAP, 8192, TCCD_MADMIT, true,
+                            TCCD_MMINB>;
 #else
 using MediumCfg = EngineCfg<512, 512, 16, 65536, 32768, 16384, false, 1>;
 #endif
@@ -331,7 +348,7 @@ Layout layout(long long n, long long mcmax, int giant_blocks, int sms) {
   Layout L;
   const long long chunk = n < kChunk ? (n > 0 ? n : 1) : kChunk;
   L.light_blocks = TCCD_LMINB * sms;
-  L.medium_blocks = sms;
+  L.medium_blocks = MediumCfg::MINB * sms;
   L.giant_blocks = giant_blocks;
   L.light_b = align256(EngineArena<LightCfg>::bytes(LightCfg::CAP));
   L.medium_b = align256(EngineArena<MediumCfg>::bytes(MediumCfg::CAP));

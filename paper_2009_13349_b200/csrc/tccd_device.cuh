@@ -38,6 +38,7 @@ struct QueryParams {
   double sep, delta, t_max;
   long long max_checks;
   int kind;
+  int tame;  // all |coordinates| < 1e300: every corner value is finite
 };
 
 // F on one axis at the 4 (u, v) corners for one time value; the lerped
@@ -60,10 +61,18 @@ __device__ __forceinline__ CornerWeights corner_weights(const Box& b) {
   return w;
 }
 
+// compare-exchange: one comparison gives both the min and the max (exact for
+// non-NaN operands; +-0 order never changes a classification or a width)
+__device__ __forceinline__ void cmpx(double a, double b, double& lo, double& hi) {
+  const bool p = a < b;
+  lo = p ? a : b;
+  hi = p ? b : a;
+}
+
 template <int KIND>
-__device__ __forceinline__ void corners_at_t(double a, double b, double c, double d,
-                                             const CornerWeights& w, double& mn, double& mx) {
-  double f00, f01, f10, f11;
+__device__ __forceinline__ void corners4(double a, double b, double c, double d,
+                                         const CornerWeights& w, double& f00, double& f01,
+                                         double& f10, double& f11) {
   if (KIND == 0) {
     const double cu0 = w.u0 * c, cu1 = w.u1 * c, dv0 = w.v0 * d, dv1 = w.v1 * d;
     f00 = a - ((w.w00 * b + cu0) + dv0);
@@ -75,31 +84,48 @@ __device__ __forceinline__ void corners_at_t(double a, double b, double c, doubl
     const double r0 = w.omv0 * c + w.v0 * d, r1 = w.omv1 * c + w.v1 * d;
     f00 = l0 - r0; f01 = l0 - r1; f10 = l1 - r0; f11 = l1 - r1;
   }
-  // min/max of binary64 values: order-free, and +-0 never changes a
-  // classification or a width, so fmin/fmax are exact.
-  mn = fmin(fmin(mn, fmin(f00, f01)), fmin(f10, f11));
-  mx = fmax(fmax(mx, fmax(f00, f01)), fmax(f10, f11));
 }
 
-// _kernel._hull_axis (_kernel.py:44-67) for one axis.
-template <int KIND, typename PtrT>
+// _kernel._hull_axis (_kernel.py:44-67) for one axis.  TAME (all corner
+// values finite): compare-exchange tournament, 10 comparisons for min and max
+// of 8 values.  Otherwise fmin/fmax from +-inf, which ignore NaN exactly like
+// the reference's `val < mn` / `val > mx` updates.
+template <int KIND, bool TAME, typename PtrT>
 __device__ __forceinline__ void hull_axis(PtrT P, int ax, double t0, double omt0, double t1,
                                           double omt1, const CornerWeights& w, double& mn,
                                           double& mx) {
   const double s0 = P[ax], s1 = P[3 + ax], s2 = P[6 + ax], s3 = P[9 + ax];
   const double e0 = P[12 + ax], e1 = P[15 + ax], e2 = P[18 + ax], e3 = P[21 + ax];
-  mn = __longlong_as_double(0x7ff0000000000000LL);   // +inf
-  mx = __longlong_as_double((long long)0xfff0000000000000ULL);  // -inf
-  corners_at_t<KIND>(omt0 * s0 + t0 * e0, omt0 * s1 + t0 * e1, omt0 * s2 + t0 * e2,
-                     omt0 * s3 + t0 * e3, w, mn, mx);
-  corners_at_t<KIND>(omt1 * s0 + t1 * e0, omt1 * s1 + t1 * e1, omt1 * s2 + t1 * e2,
-                     omt1 * s3 + t1 * e3, w, mn, mx);
+  double f[8];
+  corners4<KIND>(omt0 * s0 + t0 * e0, omt0 * s1 + t0 * e1, omt0 * s2 + t0 * e2,
+                 omt0 * s3 + t0 * e3, w, f[0], f[1], f[2], f[3]);
+  corners4<KIND>(omt1 * s0 + t1 * e0, omt1 * s1 + t1 * e1, omt1 * s2 + t1 * e2,
+                 omt1 * s3 + t1 * e3, w, f[4], f[5], f[6], f[7]);
+  if (TAME) {
+    double l0, h0, l1, h1, l2, h2, l3, h3;
+    cmpx(f[0], f[1], l0, h0);
+    cmpx(f[2], f[3], l1, h1);
+    cmpx(f[4], f[5], l2, h2);
+    cmpx(f[6], f[7], l3, h3);
+    const double la = l0 < l1 ? l0 : l1, lb = l2 < l3 ? l2 : l3;
+    const double ha = h0 > h1 ? h0 : h1, hb = h2 > h3 ? h2 : h3;
+    mn = la < lb ? la : lb;
+    mx = ha > hb ? ha : hb;
+  } else {
+    mn = __longlong_as_double(0x7ff0000000000000LL);              // +inf
+    mx = __longlong_as_double((long long)0xfff0000000000000ULL);  // -inf
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      mn = fmin(mn, f[k]);
+      mx = fmax(mx, f[k]);
+    }
+  }
 }
 
 // _kernel._classify (_kernel.py:71-94): axes x, y, z with an early return
 // at the first separated axis; hull enlarged by sep before comparing; wb is
 // the raw (unenlarged) max width, 0 when disjoint.
-template <int KIND, typename PtrT>
+template <int KIND, bool TAME, typename PtrT>
 __device__ __forceinline__ int classify_k(PtrT P, const Box& b, const double* eps, double sep,
                                           double& wb) {
   const CornerWeights w = corner_weights(b);
@@ -109,7 +135,7 @@ __device__ __forceinline__ int classify_k(PtrT P, const Box& b, const double* ep
 #pragma unroll 1
   for (int ax = 0; ax < 3; ++ax) {
     double mn, mx;
-    hull_axis<KIND>(P, ax, b.t0, omt0, b.t1, omt1, w, mn, mx);
+    hull_axis<KIND, TAME>(P, ax, b.t0, omt0, b.t1, omt1, w, mn, mx);
     const double e = eps[ax];
     const double lo = mn - sep, hi = mx + sep;
     if (lo > e || hi < -e) {
@@ -126,8 +152,21 @@ __device__ __forceinline__ int classify_k(PtrT P, const Box& b, const double* ep
 
 template <typename PtrT>
 __device__ __forceinline__ int classify(PtrT P, int kind, const Box& b, const double* eps,
-                                        double sep, double& wb) {
-  return kind == 0 ? classify_k<0>(P, b, eps, sep, wb) : classify_k<1>(P, b, eps, sep, wb);
+                                        double sep, double& wb, bool tame = false) {
+  if (tame) return kind == 0 ? classify_k<0, true>(P, b, eps, sep, wb)
+                             : classify_k<1, true>(P, b, eps, sep, wb);
+  return kind == 0 ? classify_k<0, false>(P, b, eps, sep, wb)
+                   : classify_k<1, false>(P, b, eps, sep, wb);
+}
+
+// all |coordinates| < 1e300 (and finite): lerps and corner values stay
+// below 8e300, so no comparison in the hull ever sees a NaN
+template <typename PtrT>
+__device__ __forceinline__ int tame_coords(PtrT P) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 24; ++i) ok &= fabs(P[i]) < 1e300;
+  return ok ? 1 : 0;
 }
 
 // _kernel._kappas (_kernel.py:98-132): 3 * max |F(corner + stride) - F(corner)|

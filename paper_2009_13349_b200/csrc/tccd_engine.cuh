@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         const long long cut = qp.max_checks - S.C[s] - 1;
         if (k <= cut) {
           const uint8_t head = f & kHead;
-          const int cls = classify((const double*)S.P[s], qp.kind, b, qp.eps, qp.sep, wb);
+          const int cls = classify((const double*)S.P[s], qp.kind, b, qp.eps, qp.sep, wb, qp.tame != 0);
           f = (uint8_t)cls;
           if (cls != kDisjoint) {
             int sdim; double mid; bool ph;

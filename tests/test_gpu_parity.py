@@ -84,6 +84,28 @@ def test_workload_samples_vs_oracle(cuda, config, start, count, kw):
     _vs_oracle(w, cuda, sep=kw.get("sep"), t_max=kw.get("t_max"))
 
 
+def test_extreme_coordinates_nan_path(cuda):
+    """Coordinates near the top of the binary64 range: lerps and corner values
+    overflow to +-inf and inf - inf = NaN.  The reference's hull ignores NaN
+    (its `val < mn` updates fail), which the non-tame classify path must
+    reproduce exactly; the tame fast path is only used below 1e300."""
+    from paper_2009_13349_b200 import solve_batch
+    rng = np.random.default_rng(5)
+    n = 3000
+    scale = np.where(rng.random(n) < 0.5, 1.6e308, 1e301)[:, None, None]
+    pts = (rng.random((n, 8, 3)) - 0.5) * 2 * scale
+    pts[::7] = np.clip(pts[::7] * 1e10, -1.7e308, 1.7e308)
+    kind = (rng.random(n) < 0.5).astype(np.uint8)
+    # auto filters would give eps = inf (gamma^3 overflows) and settle every
+    # query at the root; a caller FilterEps (not re-validated, solver.py:44-46)
+    # with finite eps drives the search through NaN-producing boxes
+    for eps in (None, (1e290, 1e290, 1e290), (1e300, 1e-15, 1e305)):
+        ref = oracle.solve_batch(pts, kind, 1e-6, 10_000, eps=eps)
+        got = solve_batch(torch.from_numpy(pts), torch.from_numpy(kind), max_checks=10_000,
+                          eps=eps, device=cuda, raise_on_error=False)
+        assert_same_results({k: v.numpy() for k, v in got.items()}, ref, f"extreme eps={eps}")
+
+
 def test_heavy_tail_sample_block_engine(cuda):
     from paper_2009_13349_b200 import workloads as W
     w = W.generate(2, 0, 400)
