@@ -132,7 +132,11 @@ __device__ __forceinline__ int classify_k(PtrT P, const Box& b, const double* ep
   const double omt0 = 1.0 - b.t0, omt1 = 1.0 - b.t1;
   bool contained = true;
   double width = 0.0;
+#ifdef TCCD_UNROLL_AXES
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
   for (int ax = 0; ax < 3; ++ax) {
     double mn, mx;
     hull_axis<KIND, TAME>(P, ax, b.t0, omt0, b.t1, omt1, w, mn, mx);

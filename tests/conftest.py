@@ -16,7 +16,8 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
-GOLDEN_SETS = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
+GOLDEN_SETS = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
+                     if not os.path.basename(p).startswith("ds_"))  # ds_*: dataset-format fixtures
 FIELDS = ("status", "toi", "tol", "codom", "checks", "early", "witness", "level")
 
 

@@ -248,3 +248,42 @@ def test_full_config1_properties(cuda):
     sub = {k: v.cpu().numpy()[idx] for k, v in r1.items()}
     ref = oracle.solve_batch(w.points[idx], w.kind[idx])
     assert_same_results(sub, ref, "config1 subsample")
+
+
+# --- §8(f) row 3: the benchmark harness and CLI on the GPU batch -------------
+
+@pytest.mark.parametrize("name,tag", [("handcrafted", "vf"), ("handcrafted", "ee"),
+                                      ("adv", "vf"), ("adv", "ee")])
+def test_benchmark_harness_matches_reference(cuda, name, tag):
+    """Verdicts and FP/FN/correct/early counts equal those of the reference's
+    run_benchmark(..., ("ours",)) on its own dataset files."""
+    import os
+    from conftest import GOLDEN_DIR
+    from paper_2009_13349_b200 import QueryKind
+    from paper_2009_13349_b200.benchmark import run_benchmark
+    from paper_2009_13349_b200.dataset import parse_queries
+    kind = QueryKind.VERTEX_FACE if tag == "vf" else QueryKind.EDGE_EDGE
+    g = np.load(os.path.join(GOLDEN_DIR, f"ds_{name}_{tag}.npz"))
+    rep = run_benchmark(parse_queries(os.path.join(GOLDEN_DIR, f"ds_{name}_{tag}.csv"), kind),
+                        device=cuda)
+    m = rep.method("ours")
+    assert np.array_equal(np.array(m.verdicts), g["verdicts"])
+    assert (m.fp_count, m.fn_count, m.correct_count, m.early_count) == \
+        (int(g["fp"]), int(g["fn"]), int(g["correct"]), int(g["early"]))
+    assert sum(m.histogram) == rep.size and rep.queries_per_second > 0
+
+
+def test_cli_run_and_fn_guard(cuda, tmp_path):
+    import io
+    import os
+    from conftest import GOLDEN_DIR
+    from paper_2009_13349_b200 import cli
+    from paper_2009_13349_b200.benchmark import load_report
+    out = tmp_path / "r.json"
+    rc = cli.main(["run", "--dataset", os.path.join(GOLDEN_DIR, "ds_adv_ee.csv"), "--kind", "ee",
+                   "--out", str(out)])
+    assert rc == 0 and load_report(out).method("ours").fn_count == 0
+    # a mislabeled record (far miss labeled colliding) is an FN: exit 2
+    bad = tmp_path / "bad.csv"
+    bad.write_text(("0,1,0,1,10,1,1\n" + "0,1,0,1,0,1,1\n" + "1,1,0,1,0,1,1\n" + "0,1,1,1,0,1,1\n") * 2)
+    assert cli.main(["run", "--dataset", str(bad), "--kind", "vf", "--format", "csv"]) == 2
