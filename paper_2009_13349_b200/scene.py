@@ -1,0 +1,451 @@
+"""Mesh-level callers of the solver, batched on the GPU.
+
+Same API and results as the reference's scene module
+(pkg/src/ccdkit/scene.py): the broad phase produces exactly the reference's
+candidate set, in its order, and the narrow phase runs as batched
+``solve_batch`` calls instead of one ``solve`` per candidate:
+
+* ``construct_active_set`` (:303-327): one batched solve over all
+  candidates.
+* ``line_search_step`` (:468-583): the reference solves candidates in order
+  on a shrinking interval [0, alpha] (each solve's t_max is the alpha left by
+  the candidates before it).  That order dependence is reproduced exactly:
+  a batch is solved at the current alpha, accepted up to the first candidate
+  that lowers alpha, and only the candidates after it are re-solved at the
+  new alpha -- one batched solve per alpha decrease instead of one solve
+  per candidate.  Non-dyadic t_max goes through the engine's general
+  ordering path.
+
+The broad phase itself runs on the host (a GPU version is §8(f) row 2).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+import torch
+
+from .core import DomainBox, Query, QueryKind, SolverConfig
+from .inclusion import compute_filters, compute_gamma
+from .solver import solve_batch
+
+_SQRT3 = math.sqrt(3.0)
+_DISTANCE_SLACK = 1e-9  # scene.py:42-45
+
+
+def edges_from_triangles(triangles) -> np.ndarray:
+    tris = np.asarray(triangles, dtype=np.intp)
+    if tris.size == 0:
+        return np.zeros((0, 2), dtype=np.intp)
+    if tris.ndim != 2 or tris.shape[1] != 3:
+        raise ValueError("triangles must be an (m, 3) index array")
+    e = np.concatenate((tris[:, (0, 1)], tris[:, (1, 2)], tris[:, (2, 0)]))
+    e.sort(axis=1)
+    return np.unique(e, axis=0)
+
+
+@dataclass(frozen=True)
+class TriMeshPair:
+    """Triangle mesh with vertex positions at both ends of one step
+    (scene.py:68-114, same validation)."""
+
+    x0: np.ndarray
+    x1: np.ndarray
+    triangles: np.ndarray
+    edges: np.ndarray | None = None
+
+    def __post_init__(self):
+        x0 = np.ascontiguousarray(np.asarray(self.x0, dtype=np.float64))
+        x1 = np.ascontiguousarray(np.asarray(self.x1, dtype=np.float64))
+        if x0.ndim != 2 or x0.shape[1] != 3 or x1.shape != x0.shape:
+            raise ValueError("x0 and x1 must be (n, 3) arrays of equal shape")
+        if not (np.all(np.isfinite(x0)) and np.all(np.isfinite(x1))):
+            raise ValueError("vertex positions must be finite")
+        tris = np.ascontiguousarray(np.asarray(self.triangles, dtype=np.intp))
+        if tris.size == 0:
+            tris = np.zeros((0, 3), dtype=np.intp)
+        if tris.ndim != 2 or tris.shape[1] != 3:
+            raise ValueError("triangles must be an (m, 3) index array")
+        if self.edges is None:
+            edges = edges_from_triangles(tris)
+        else:
+            edges = np.ascontiguousarray(np.asarray(self.edges, dtype=np.intp))
+            if edges.size == 0:
+                edges = np.zeros((0, 2), dtype=np.intp)
+            if edges.ndim != 2 or edges.shape[1] != 2:
+                raise ValueError("edges must be a (k, 2) index array")
+        n = x0.shape[0]
+        for name, idx in (("triangles", tris), ("edges", edges)):
+            if idx.size and (int(idx.min()) < 0 or int(idx.max()) >= n):
+                raise ValueError(f"{name} index vertices outside [0, {n})")
+        object.__setattr__(self, "x0", x0)
+        object.__setattr__(self, "x1", x1)
+        object.__setattr__(self, "triangles", tris)
+        object.__setattr__(self, "edges", edges)
+
+    @property
+    def n_vertices(self) -> int:
+        return int(self.x0.shape[0])
+
+    def at(self, alpha: float) -> np.ndarray:
+        return self.x0 + float(alpha) * (self.x1 - self.x0)
+
+
+@dataclass(frozen=True)
+class ContactCandidate:
+    kind: QueryKind
+    indices: tuple
+    query: Query
+
+
+@dataclass
+class CandidateSet:
+    """Broad-phase output in batch layout, reference order (VF pairs sorted
+    by (vertex, triangle), then EE pairs sorted by (edge_a, edge_b))."""
+
+    kind: np.ndarray     # [m] u8
+    indices: np.ndarray  # [m, 2] int64
+    points: np.ndarray   # [m, 8, 3] f64
+
+    @property
+    def m(self) -> int:
+        return int(self.kind.shape[0])
+
+    def candidate(self, i: int) -> ContactCandidate:
+        q = Query(QueryKind(int(self.kind[i])), tuple(map(tuple, self.points[i, :4])),
+                  tuple(map(tuple, self.points[i, 4:])))
+        return ContactCandidate(QueryKind(int(self.kind[i])),
+                                (int(self.indices[i, 0]), int(self.indices[i, 1])), q)
+
+    def to_list(self) -> list:
+        return [self.candidate(i) for i in range(self.m)]
+
+
+def _boxes(mesh: TriMeshPair, idx: np.ndarray, inflation: float):
+    pts = np.stack((mesh.x0[idx], mesh.x1[idx]))  # (2, m, k, 3), scene.py:195-200
+    return pts.min(axis=(0, 2)) - inflation, pts.max(axis=(0, 2)) + inflation
+
+
+def load_obj(path) -> tuple[np.ndarray, np.ndarray]:
+    """Positions and triangles of a Wavefront OBJ file (scene.py:117-149):
+    ``v`` and ``f`` records only, polygons fan-triangulated, ``v/vt/vn``
+    groups keep the vertex index, negative indices count back."""
+    verts, faces = [], []
+    with open(path, encoding="utf-8") as fh:
+        for line_no, raw in enumerate(fh, start=1):
+            tok = raw.split()
+            if not tok or tok[0].startswith("#"):
+                continue
+            if tok[0] == "v":
+                if len(tok) < 4:
+                    raise ValueError(f"line {line_no}: vertex needs 3 coordinates")
+                verts.append([float(t) for t in tok[1:4]])
+            elif tok[0] == "f":
+                if len(tok) < 4:
+                    raise ValueError(f"line {line_no}: face needs >= 3 corners")
+                ids = [int(t.split("/", 1)[0]) for t in tok[1:]]
+                ids = [i - 1 if i > 0 else len(verts) + i for i in ids]
+                faces += [[ids[0], ids[k], ids[k + 1]] for k in range(1, len(ids) - 1)]
+    v = np.asarray(verts, dtype=np.float64).reshape(-1, 3)
+    f = np.asarray(faces, dtype=np.intp).reshape(-1, 3)
+    if f.size and (f.min() < 0 or f.max() >= len(v)):
+        raise ValueError("face index out of range")
+    return v, f
+
+
+def _overlapping_pairs(alo, ahi, blo, bhi):
+    """All (a, b) whose closed boxes overlap on every axis.
+
+    Sweep on x: b sorted by lower x bound; for each a the window is the b
+    with blo_x <= ahi_x and blo_x >= alo_x - 2*max_width (a superset of
+    bhi_x >= alo_x), then the exact test on all three axes."""
+    if len(alo) == 0 or len(blo) == 0:
+        return np.zeros((0, 2), dtype=np.int64)
+    order = np.argsort(blo[:, 0], kind="stable")
+    bstart = blo[order, 0]
+    wmax = float(np.max(bhi[:, 0] - blo[:, 0]))
+    hi_i = np.searchsorted(bstart, ahi[:, 0], side="right")
+    lo_i = np.minimum(np.searchsorted(bstart, alo[:, 0] - 2.0 * wmax, side="left"), hi_i)
+    cnt = hi_i - lo_i
+    a_rep = np.repeat(np.arange(len(alo)), cnt)
+    start = np.repeat(lo_i - (np.cumsum(cnt) - cnt), cnt)
+    b_rep = order[np.arange(len(a_rep)) + start]
+    ok = np.ones(len(a_rep), dtype=bool)
+    for k in range(3):
+        ok &= (alo[a_rep, k] <= bhi[b_rep, k]) & (blo[b_rep, k] <= ahi[a_rep, k])
+    return np.stack([a_rep[ok], b_rep[ok]], 1).astype(np.int64)
+
+
+def broad_phase_batch(mesh: TriMeshPair, inflation: float = 0.0) -> CandidateSet:
+    """Exactly the pairs of the reference broad phase (scene.py:225-300):
+    primitives whose inflated swept boxes overlap, minus pairs that share a
+    mesh vertex.  (The reference's grid hash is a superset filter followed by
+    the same exact box test, so its result is this set.)"""
+    if not (inflation >= 0.0 and math.isfinite(inflation)):
+        raise ValueError("inflation must be >= 0 and finite")
+    n = mesh.n_vertices
+    empty = CandidateSet(np.zeros(0, np.uint8), np.zeros((0, 2), np.int64),
+                         np.zeros((0, 8, 3)))
+    if n == 0:
+        return empty
+    vlo, vhi = _boxes(mesh, np.arange(n, dtype=np.intp)[:, None], inflation)
+    tris, edges = mesh.triangles, mesh.edges
+    kinds, idxs, pts = [], [], []
+    if len(tris):
+        tlo, thi = _boxes(mesh, tris, inflation)
+        pr = _overlapping_pairs(vlo, vhi, tlo, thi)
+        keep = ~np.any(tris[pr[:, 1]] == pr[:, 0:1], axis=1)
+        pr = pr[keep]
+        pr = pr[np.lexsort((pr[:, 1], pr[:, 0]))]
+        if len(pr):
+            v, t = pr[:, 0], tris[pr[:, 1]]
+            vid = np.stack([v, t[:, 0], t[:, 1], t[:, 2]], 1)
+            kinds.append(np.zeros(len(pr), np.uint8))
+            idxs.append(pr)
+            pts.append(np.concatenate([mesh.x0[vid], mesh.x1[vid]], 1))
+    if len(edges):
+        elo, ehi = _boxes(mesh, edges, inflation)
+        pr = _overlapping_pairs(elo, ehi, elo, ehi)
+        pr = pr[pr[:, 0] < pr[:, 1]]
+        a, b = edges[pr[:, 0]], edges[pr[:, 1]]
+        share = (a[:, 0] == b[:, 0]) | (a[:, 0] == b[:, 1]) | (a[:, 1] == b[:, 0]) | \
+            (a[:, 1] == b[:, 1])
+        pr = pr[~share]
+        pr = pr[np.lexsort((pr[:, 1], pr[:, 0]))]
+        if len(pr):
+            a, b = edges[pr[:, 0]], edges[pr[:, 1]]
+            vid = np.stack([a[:, 0], a[:, 1], b[:, 0], b[:, 1]], 1)
+            kinds.append(np.ones(len(pr), np.uint8))
+            idxs.append(pr)
+            pts.append(np.concatenate([mesh.x0[vid], mesh.x1[vid]], 1))
+    if not kinds:
+        return empty
+    return CandidateSet(np.concatenate(kinds), np.concatenate(idxs),
+                        np.ascontiguousarray(np.concatenate(pts)))
+
+
+def broad_phase(mesh: TriMeshPair, inflation: float = 0.0) -> list:
+    """Reference-shaped result: a list of ContactCandidate."""
+    return broad_phase_batch(mesh, inflation).to_list()
+
+
+def _solve(cs: CandidateSet, sel, cfg: SolverConfig, separation, device):
+    pts = torch.from_numpy(np.ascontiguousarray(cs.points[sel]))
+    kind = torch.from_numpy(np.ascontiguousarray(cs.kind[sel]))
+    sep = separation if np.isscalar(separation) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(separation, dtype=np.float64)))
+    r = solve_batch(pts, kind, cfg, separation=sep, device=device)
+    return {k: v.numpy() for k, v in r.items()}
+
+
+def _witness(r, i) -> DomainBox:
+    w = r["witness"][i]
+    return DomainBox((float(w[0]), float(w[1])), (float(w[2]), float(w[3])),
+                     (float(w[4]), float(w[5])), int(r["level"][i]))
+
+
+def construct_active_set(mesh: TriMeshPair, delta: float = 1e-6, max_checks: int = 1_000_000,
+                         separation: float = 0.0, device=None) -> list:
+    """Candidates the solver could not rule out, with toi and witness
+    (scene.py:303-327), from one batched solve."""
+    cs = broad_phase_batch(mesh, inflation=separation + delta)
+    if cs.m == 0:
+        return []
+    cfg = SolverConfig(delta=delta, max_checks=max_checks, separation=separation)
+    r = _solve(cs, slice(None), cfg, separation, device)
+    hits = np.flatnonzero(r["status"] == 1)
+    return [(cs.candidate(i), float(r["toi"][i]), _witness(r, i)) for i in hits]
+
+
+# --- start-distance lower bounds: the reference's closed forms (scene.py:335-419),
+# same operation order (dot products left to right, Vec3 arithmetic per component)
+
+def _sub(a, b):
+    return (a[0] - b[0], a[1] - b[1], a[2] - b[2])
+
+
+def _add(a, b):
+    return (a[0] + b[0], a[1] + b[1], a[2] + b[2])
+
+
+def _scl(a, s):
+    return (a[0] * s, a[1] * s, a[2] * s)
+
+
+def _dot(a, b):
+    return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]
+
+
+def _cross(a, b):
+    return (a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0])
+
+
+def _norm(v):
+    return math.sqrt(_dot(v, v))
+
+
+def _clamp01(s):
+    return 0.0 if s < 0.0 else (1.0 if s > 1.0 else s)
+
+
+def _pt_seg(p, a, b):
+    ab = _sub(b, a)
+    denom = _dot(ab, ab)
+    if denom == 0.0:
+        return _norm(_sub(p, a))
+    s = _clamp01(_dot(_sub(p, a), ab) / denom)
+    return _norm(_sub(p, _add(a, _scl(ab, s))))
+
+
+def _pt_tri(p, a, b, c):
+    best = min(_pt_seg(p, a, b), _pt_seg(p, b, c), _pt_seg(p, c, a))
+    n = _cross(_sub(b, a), _sub(c, a))
+    nn = _dot(n, n)
+    if nn > 0.0:
+        w0 = _dot(_cross(_sub(c, b), _sub(p, b)), n)
+        w1 = _dot(_cross(_sub(a, c), _sub(p, c)), n)
+        w2 = _dot(_cross(_sub(b, a), _sub(p, a)), n)
+        if w0 >= 0.0 and w1 >= 0.0 and w2 >= 0.0:
+            best = min(best, abs(_dot(_sub(p, a), n)) / math.sqrt(nn))
+    return best
+
+
+def _seg_seg(p1, q1, p2, q2):
+    d1, d2, r = _sub(q1, p1), _sub(q2, p2), _sub(p1, p2)
+    a, e, f = _dot(d1, d1), _dot(d2, d2), _dot(d2, r)
+    if a == 0.0 and e == 0.0:
+        return _norm(r)
+    if a == 0.0:
+        s, t = 0.0, _clamp01(f / e)
+    else:
+        c = _dot(d1, r)
+        if e == 0.0:
+            t, s = 0.0, _clamp01(-c / a)
+        else:
+            b = _dot(d1, d2)
+            denom = a * e - b * b
+            s = _clamp01((b * f - c * e) / denom) if denom > 0.0 else 0.0
+            t = (b * s + f) / e
+            if t < 0.0:
+                t, s = 0.0, _clamp01(-c / a)
+            elif t > 1.0:
+                t, s = 1.0, _clamp01((b - c) / a)
+    return _norm(_sub(_add(p1, _scl(d1, s)), _add(p2, _scl(d2, t))))
+
+
+def distance_lb(kind: int, points8: np.ndarray) -> float:
+    """primitive_distance_lb (scene.py:404-419) on one candidate's points."""
+    p = [tuple(float(c) for c in points8[k]) for k in range(4)]
+    d = _pt_tri(*p) if kind == 0 else _seg_seg(*p)
+    if d <= 0.0:
+        return 0.0
+    return max(0.0, math.nextafter(d / _SQRT3, 0.0))
+
+
+def primitive_distance_lb(candidate: ContactCandidate) -> float:
+    return distance_lb(int(candidate.kind), candidate.query.all_coordinates())
+
+
+class InfeasibleStepError(RuntimeError):
+    """No positive step fraction can be certified (scene.py:422-430)."""
+
+
+@dataclass(frozen=True)
+class CandidateBound:
+    candidate: ContactCandidate
+    distance_lb: float
+    separation: float
+    toi: float | None
+    witness: DomainBox | None
+
+
+@dataclass(frozen=True)
+class LineSearchResult:
+    alpha: float
+    p: float
+    validations: int
+    bounds: tuple
+    limiting: int | None
+
+    @property
+    def limiting_bound(self):
+        return None if self.limiting is None else self.bounds[self.limiting]
+
+
+def line_search_step(mesh: TriMeshPair, *, p: float, delta: float = 1e-6,
+                     max_checks: int = 1_000_000,
+                     energy_decreases: Callable[[float], bool] | None = None,
+                     alpha_min: float = 1e-8, inflation: float | None = None,
+                     device=None) -> LineSearchResult:
+    """Largest certified collision-free step fraction (scene.py:468-583)."""
+    if not (0.0 < p < 1.0):
+        raise ValueError("p must lie strictly between 0 and 1")
+    if inflation is None:
+        inflation = 2.0 * delta
+    cs = broad_phase_batch(mesh, inflation)
+    m = cs.m
+    d_lb = np.empty(m)
+    eps_max = np.empty(m)
+    for i in range(m):
+        d_lb[i] = distance_lb(int(cs.kind[i]), cs.points[i])
+        if d_lb[i] <= 0.0:
+            raise InfeasibleStepError(
+                f"{QueryKind(int(cs.kind[i])).name} pair {tuple(int(x) for x in cs.indices[i])} "
+                "touches at the step start; no positive step can be certified")
+        fe = compute_filters(QueryKind(int(cs.kind[i])), compute_gamma(cs.points[i]),
+                             separation=min(p * d_lb[i], delta))
+        eps_max[i] = max(fe.eps)
+
+    def worst_ratio(tol):
+        return min((float(d) - tol - float(e) - _DISTANCE_SLACK) / float(d)
+                   for d, e in zip(d_lb, eps_max))
+
+    alpha, validations, bounds, limiting = 1.0, 0, [], None
+    tol_assumed = delta
+    while m:
+        validations += 1
+        worst = worst_ratio(tol_assumed)
+        while p >= worst:
+            p *= 0.5
+            if p == 0.0:
+                raise InfeasibleStepError("validation halved p to zero; the start distances "
+                                          "cannot cover the solver tolerance plus numeric error")
+        seps = [min(p * float(d), delta) for d in d_lb]
+        alpha, achieved, limiting = 1.0, tol_assumed, None
+        bounds = []
+        i0 = 0
+        while i0 < m:
+            # candidates i0.. solved at the current alpha; results hold until
+            # the first one that lowers alpha
+            cfg = SolverConfig(delta=tol_assumed, max_checks=max_checks, t_max=alpha)
+            r = _solve(cs, slice(i0, m), cfg, seps[i0:], device)
+            nxt = m
+            for k in range(i0, m):
+                j = k - i0
+                hit = r["status"][j] == 1
+                toi = float(r["toi"][j]) if hit else None
+                # a free result carries codomain width 0 (solver.py:89-93)
+                achieved = max(achieved, float(r["codom"][j]) if hit else 0.0)
+                bounds.append(CandidateBound(cs.candidate(k), float(d_lb[k]), seps[k], toi,
+                                             _witness(r, j) if hit else None))
+                if hit and toi < alpha:
+                    alpha = toi
+                    limiting = len(bounds) - 1
+                    nxt = k + 1
+                    break
+            if alpha == 0.0:
+                break  # the remaining interval is empty
+            i0 = nxt
+        if not (achieved > tol_assumed):
+            break
+        if p < worst_ratio(achieved):
+            break
+        tol_assumed = achieved
+    if energy_decreases is not None:
+        while alpha > alpha_min and not energy_decreases(alpha):
+            alpha *= 0.5
+    return LineSearchResult(alpha=alpha, p=p, validations=validations, bounds=tuple(bounds),
+                            limiting=limiting)
