@@ -40,7 +40,6 @@
 
 namespace tccd {
 
-constexpr uint8_t kPNone = 0xFF;
 constexpr int kIntMax = 0x7fffffff;
 constexpr uint8_t kClassified = 64;  // flag bit: box already classified
 constexpr uint8_t kHead = 128;       // flag bit: first box of a run of equal t_lo
@@ -63,8 +62,6 @@ struct EngineCfg {
   static constexpr int ADMIT = ADMIT_;  // admit below this fill (0: = cap)
   static constexpr bool SMEM = SMEM_;   // per-box bookkeeping in shared memory
   static constexpr int MINB = MINB_;    // CTAs per SM (launch bounds)
-  using Off = typename std::conditional<(CAP_ > 0 && CAP_ <= 32768), unsigned short,
-                                        unsigned int>::type;
 };
 
 template <int G>
@@ -92,60 +89,6 @@ __device__ __forceinline__ unsigned long long group_excl_scan(unsigned long long
     return block_excl_scan<G>(v, sw, total);
   }
 }
-
-// Byte reads from a 16-byte-aligned array through a one-vector cache: a
-// thread walking a contiguous chunk issues one 16-byte load per 16 boxes
-// (used where the per-box bookkeeping lives in global memory).
-template <bool VEC>
-struct ByteVecReader {
-  const uint8_t* p;
-  int base;
-  uint4 v;
-  __device__ __forceinline__ explicit ByteVecReader(const uint8_t* q) : p(q), base(-1) {}
-  __device__ __forceinline__ uint8_t operator()(int i) {
-    if constexpr (!VEC) {
-      return p[i];
-    } else {
-      const int b = i & ~15;  // (16-byte aligned chunk of bytes)
-      if (b != base) {
-        base = b;
-        v = *reinterpret_cast<const uint4*>(p + b);
-      }
-      const int k = (i >> 2) & 3;
-      const unsigned w = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
-      return (uint8_t)(w >> ((i & 3) * 8));
-    }
-  }
-};
-
-// same for 16-bit / 32-bit offsets (a 16-byte vector holds 8 / 4 of them)
-template <bool VEC, typename T>
-struct OffVecReader {
-  static constexpr int PER = 16 / (int)sizeof(T);
-  const T* p;
-  int base;
-  uint4 v;
-  __device__ __forceinline__ explicit OffVecReader(const T* q) : p(q), base(-1) {}
-  __device__ __forceinline__ int operator()(int i) {
-    if constexpr (!VEC) {
-      return (int)p[i];
-    } else {
-      const int b = i & ~(PER - 1);
-      if (b != base) {
-        base = b;
-        v = *reinterpret_cast<const uint4*>(p + b);
-      }
-      const int e = i & (PER - 1);
-      if constexpr (sizeof(T) == 4) {
-        return (int)(e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w)));
-      } else {
-        const int k = e >> 1;
-        const unsigned w = k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
-        return (int)((w >> ((e & 1) * 16)) & 0xffffu);
-      }
-    }
-  }
-};
 
 // two exclusive sums over a group in one pass (shared barriers)
 template <int G>
@@ -279,10 +222,26 @@ __device__ __forceinline__ int group_scan_excl_int(int v, int ident, int* swi) {
   }
 }
 
+// Per-chunk bookkeeping of a level list: one entry per 32 consecutive boxes
+// (one warp's boxes in P1).  Masks (bit = box of the chunk): refining (non-
+// disjoint, not accepted), second A child (u/v split with an upper child),
+// B child (t split), run head.  Bases: exclusive prefixes over the list of
+// A children, B children and refining boxes at the chunk start; M = refining
+// count before the last run head before the chunk, N = refining count
+// before the first run head after the chunk (the list total if none).
+// Any box's prefixes are then O(1): base + popc(mask & lanes below).
+struct Chunks {
+  unsigned int* m[4];  // R, U, T, H
+  int* c[5];           // A, B, P, M, N
+};
+constexpr int kMR = 0, kMU = 1, kMT = 2, kMH = 3;
+constexpr int kCA = 0, kCB = 1, kCP = 2, kCM = 3, kCN = 4;
+
+__device__ __forceinline__ unsigned int lowmask(int k) { return (1u << k) - 1u; }  // k < 32
+
 // global arena of one group
 template <class Cfg>
 struct EngineArena {
-  using Off = typename Cfg::Off;
   Box* box[2];
   double* wb[2];
   unsigned int* ref[2];
@@ -292,17 +251,18 @@ struct EngineArena {
   unsigned long long* bkey;  // [cap]
   unsigned int* bpush;
   unsigned int* bref;
-  // per-box bookkeeping when it lives in global memory
+  // per-box / per-chunk bookkeeping when it lives in global memory
   uint8_t* slot_of[2];
   uint8_t* flag[2];
-  Off* offA;
-  Off* offB;
+  Chunks ch;
+
+  __host__ __device__ static long long chunks(long long cap) { return cap / 32 + 1; }
 
   __host__ __device__ static size_t bytes(long long cap) {
     size_t b = 2 * align256(cap * sizeof(Box)) + 2 * align256(cap * 8) + 2 * align256(cap * 4) +
                align256(2 * cap * 8) + 2 * align256(2 * cap * 4) + align256(cap * 8) +
                2 * align256(cap * 4);
-    if (!Cfg::SMEM) b += 4 * align256(cap) + 2 * align256(cap * sizeof(Off));
+    if (!Cfg::SMEM) b += 4 * align256(cap) + 9 * align256(chunks(cap) * 4);
     return b;
   }
 
@@ -320,8 +280,8 @@ struct EngineArena {
     if (!Cfg::SMEM) {
       for (int k = 0; k < 2; ++k) { slot_of[k] = base + o; o += align256(cap); }
       for (int k = 0; k < 2; ++k) { flag[k] = base + o; o += align256(cap); }
-      offA = (Off*)(base + o); o += align256(cap * sizeof(Off));
-      offB = (Off*)(base + o); o += align256(cap * sizeof(Off));
+      for (int k = 0; k < 4; ++k) { ch.m[k] = (unsigned int*)(base + o); o += align256(chunks(cap) * 4); }
+      for (int k = 0; k < 5; ++k) { ch.c[k] = (int*)(base + o); o += align256(chunks(cap) * 4); }
     }
   }
 };
@@ -349,11 +309,11 @@ struct EngineShared {
   uint8_t cont[Q];       // 1: children kept; 2: deferred; 3: evicted (children counted)
   uint8_t unsorted[Q];
   uint8_t uniform[Q];    // dyadic t_max: every level has uniform widths (closed-form order)
-  int segP0[Q];          // flat count of refining boxes before the segment
+  int segP0[Q], segP1[Q];  // flat count of refining boxes before / after the segment
   unsigned long long sw[2 * (Cfg::G / 32)];
   int swi[4 * (Cfg::G / 32)];
   int any_general;
-  int n_cur, n_next, admit_k, exhausted, A_tot, B_tot, rot;
+  int n_cur, n_next, admit_k, exhausted, A_tot, B_tot, P_tot, rot;
   unsigned long long deferred;
   int deferred_last;     // queries deferred in the previous round
   long long admit_base;
@@ -362,10 +322,13 @@ struct EngineShared {
 
 template <class Cfg>
 struct EngineSmemBoxes {
-  static constexpr int CAP = Cfg::SMEM ? Cfg::CAP : 1;
+  static constexpr int CAP = Cfg::SMEM ? Cfg::CAP : 32;
+  static_assert(CAP % 32 == 0, "level lists are whole chunks");
+  static constexpr int CH = CAP / 32;
+  unsigned int m[4][CH];
+  int c[5][CH];
   uint8_t slot_of[2][CAP];
   uint8_t flag[2][CAP];
-  typename Cfg::Off offA[CAP], offB[CAP];
 };
 
 // shared memory of ONE group (16-byte aligned); a CTA holds NT / G groups
@@ -437,7 +400,6 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   // another (G = 32: warp-synchronous, no block barriers).
   constexpr int G = Cfg::G, Q = Cfg::Q;
   constexpr int NT = G;  // stride of the per-group loops
-  using Off = typename Cfg::Off;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int group = threadIdx.x / G;
   unsigned char* gsmem = smem_raw + (size_t)group * engine_smem_bytes<Cfg>();
@@ -446,18 +408,19 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   ar.init(io.arenas + ((size_t)blockIdx.x * (Cfg::NT / G) + group) * io.arena_bytes, io.cap);
   uint8_t* slot_of[2];
   uint8_t* flags[2];
-  Off* offA;
-  Off* offB;
+  Chunks ch;
   if (Cfg::SMEM) {
     auto* SB = reinterpret_cast<EngineSmemBoxes<Cfg>*>(gsmem + sizeof(EngineShared<Cfg>));
     slot_of[0] = SB->slot_of[0]; slot_of[1] = SB->slot_of[1];
     flags[0] = SB->flag[0]; flags[1] = SB->flag[1];
-    offA = SB->offA; offB = SB->offB;
+    for (int k = 0; k < 4; ++k) ch.m[k] = SB->m[k];
+    for (int k = 0; k < 5; ++k) ch.c[k] = SB->c[k];
   } else {
     slot_of[0] = ar.slot_of[0]; slot_of[1] = ar.slot_of[1];
     flags[0] = ar.flag[0]; flags[1] = ar.flag[1];
-    offA = ar.offA; offB = ar.offB;
+    ch = ar.ch;
   }
+  const int lane = threadIdx.x & 31;
   const int cap = Cfg::CAP ? Cfg::CAP : (int)io.cap;
   const int qcap = Cfg::QCAP ? Cfg::QCAP : cap;
   const int admit_lim = Cfg::ADMIT ? Cfg::ADMIT : cap;
@@ -683,7 +646,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     if (!(r_cur & kRefRoot)) p_cur = bprev[r_cur & kRefSrcMask];
     else if ((r_cur & kRefExt) == kRefExt) p_cur = pool[r_cur & kRefSrcMask];
     unsigned int r_nxt = tid + NT < n ? rf[tid + NT] : kRefRoot;
-    for (int i = tid; i < n; i += NT) {
+    // (warp-uniform trip count: every lane reaches the chunk ballots)
+    for (int i = tid; i - lane < n; i += NT) {
       Box p_nxt;
       if (!(r_nxt & kRefRoot)) p_nxt = bprev[r_nxt & kRefSrcMask];
       else if ((r_nxt & kRefExt) == kRefExt) p_nxt = pool[r_nxt & kRefSrcMask];
@@ -693,11 +657,12 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       r_cur = r_nxt;
       p_cur = p_nxt;
       r_nxt = r_nn;
+      uint8_t f = 0;
+      if (i < n) {
       const int s = sl[i];
-      if (s == kPNone) continue;
       const QueryParams& qp = S.qp[s];
       Box b;
-      uint8_t f = fl[i];  // head bit (+ class, for roots and deferred boxes)
+      f = fl[i];  // head bit (+ class, for roots and deferred boxes)
       double wb = 0.0;
       if ((r & kRefExt) == kRefExt) {
         b = p;  // handed over (unclassified)
@@ -741,6 +706,23 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         if (f & 4) atomicMin(&S.acc[s], k);
       }
       fl[i] = f;
+      }  // i < n
+      // chunk masks (f = 0 past the end: disjoint, no head)
+      {
+        const bool refine = (f & 3) != kDisjoint && !(f & 4);
+        const int sd = (f >> 3) & 3;
+        const unsigned int mr = __ballot_sync(0xffffffffu, refine);
+        const unsigned int mu = __ballot_sync(0xffffffffu, refine && sd != 0 && (f & 32));
+        const unsigned int mt = __ballot_sync(0xffffffffu, refine && sd == 0);
+        const unsigned int mh = __ballot_sync(0xffffffffu, (f & kHead) != 0);
+        if (lane == 0) {
+          const int c = (i - lane) >> 5;
+          ch.m[kMR][c] = mr;
+          ch.m[kMU][c] = mu;
+          ch.m[kMT][c] = mt;
+          ch.m[kMH][c] = mh;
+        }
+      }
     }
     gsync<G>();
     TCCD_PHASE(3);
@@ -808,81 +790,64 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     }
     gsync<G>();
     TCCD_PHASE(4);
-    // ================= P4: child counts -> flat prefixes (A, B, refining boxes P)
-    // Threads own contiguous chunks.  For uniform queries (dyadic t_max) the
-    // next level's order is closed-form (see P4c); the run carries M (P at the
-    // head of the current run) and N (P at the next head) come from a
-    // forward max-scan and a reverse min-scan over the chunks.
-    // (global-memory bookkeeping: 16-box aligned chunks for vector loads)
-    const int c4 = Cfg::SMEM ? (n + NT - 1) / NT : (((n + NT - 1) / NT + 15) & ~15);
-    const int lo4 = tid * c4 < n ? tid * c4 : n;
-    const int hi4 = lo4 + c4 < n ? lo4 + c4 : n;
-    int P_end, A_end, carryN;
+    // ================= P4: chunk scan -> flat prefixes (A, B, refining boxes P)
+    // Threads own contiguous ranges of 32-box chunks (one or two chunks each
+    // in the shared-memory tiers).  Every query's boxes are counted (also
+    // finished ones): positions are segment-relative, so that only shifts the
+    // flat numbering.  The run carries M / N come from a forward max-scan and
+    // a reverse min-scan of the chunks' run heads.
     {
+      const int nch = (n + 31) >> 5;
+      const int cpt = (nch + NT - 1) / NT;
+      const int c0 = tid * cpt < nch ? tid * cpt : nch;
+      const int c1 = c0 + cpt < nch ? c0 + cpt : nch;
       unsigned int sA = 0, sB = 0;
       int sP = 0, lastHeadP = -1, firstHeadP = -1;
-      bool general = false;
-      // (segments are contiguous: per-query values are cached while a
-      // chunk stays inside one segment)
-      int cs = -1;
-      bool c_cont = false, c_uni = false;
-      ByteVecReader<!Cfg::SMEM> rsl(sl), rfl(fl);
-      for (int i = lo4; i < hi4; ++i) {
-        const int s = rsl(i);
-        if (s == kPNone) continue;
-        if (s != cs) { cs = s; c_cont = S.cont[s] != 0; c_uni = S.uniform[s] != 0; }
-        const uint8_t f = rfl(i);
-        if (f & kHead) { if (firstHeadP < 0) firstHeadP = sP; lastHeadP = sP; }
-        if (!c_cont) continue;
-        general |= !c_uni;
-        // (boxes before j are disjoint, so they never refine)
-        if ((f & 3) == kDisjoint || (f & 4)) continue;
-        const int sdim = (f >> 3) & 3;
-        sA += 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
-        sB += sdim == 0 ? 1 : 0;
-        sP += 1;
+      for (int c = c0; c < c1; ++c) {
+        const unsigned int R = ch.m[kMR][c], H = ch.m[kMH][c];
+        if (H) {
+          if (firstHeadP < 0) firstHeadP = sP + __popc(R & lowmask(__ffs(H) - 1));
+          lastHeadP = sP + __popc(R & lowmask(31 - __clz(H)));
+        }
+        const int pr = __popc(R);
+        sP += pr;
+        sA += pr + __popc(ch.m[kMU][c]);
+        sB += __popc(ch.m[kMT][c]);
       }
-      if (general) S.any_general = 1;
       unsigned long long pre, preP, tot, totP;
       group_excl_scan2<G>(((unsigned long long)sA << 32) | sB, (unsigned long long)sP, S.sw, pre,
                           preP, tot, totP);
       const int P0 = (int)preP;
-      int carryM;
+      int carryM, carryN;
       group_scan_maxfwd_minrev<G>(lastHeadP >= 0 ? P0 + lastHeadP : -1,
                                   firstHeadP >= 0 ? P0 + firstHeadP : kIntMax, S.swi, carryM,
                                   carryN);
       if (carryN == kIntMax) carryN = (int)totP;
-      unsigned int Ar = (unsigned int)(pre >> 32), Br = (unsigned int)(pre & 0xffffffffu);
-      int Pr = P0, M = carryM;
-      if (tid == 0) { S.A_tot = (int)(tot >> 32); S.B_tot = (int)(tot & 0xffffffffu); }
-      ByteVecReader<!Cfg::SMEM> rsl2(sl), rfl2(fl);
-      cs = -1;
-      int c_off = 0, c_last = 0;
-      for (int i = lo4; i < hi4; ++i) {
-        const int s = rsl2(i);
-        if (s == kPNone) continue;
-        if (s != cs) {
-          cs = s;
-          c_off = S.seg_off[s];
-          c_last = c_off + S.seg_n[s] - 1;
-          c_cont = S.cont[s] != 0;
-          c_uni = S.uniform[s] != 0;
-        }
-        const uint8_t f = rfl2(i);
-        if (f & kHead) M = Pr;
-        if (i == c_off) { S.segA0[s] = (int)Ar; S.segB0[s] = (int)Br; S.segP0[s] = Pr; }
-        offA[i] = c_uni ? (Off)M : (Off)Ar;  // uniform: run-start carry
-        offB[i] = (Off)Br;
-        if (c_cont && (f & 3) != kDisjoint && !(f & 4)) {
-          const int sdim = (f >> 3) & 3;
-          Ar += 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
-          Br += sdim == 0 ? 1 : 0;
-          Pr += 1;
-        }
-        if (i == c_last) { S.segA1[s] = (int)Ar; S.segB1[s] = (int)Br; }
+      if (tid == 0) {
+        S.A_tot = (int)(tot >> 32);
+        S.B_tot = (int)(tot & 0xffffffffu);
+        S.P_tot = (int)totP;
+        S.any_general = 0;
       }
-      P_end = Pr;
-      A_end = (int)Ar;
+      int Ar = (int)(pre >> 32), Br = (int)(pre & 0xffffffffu), Pr = P0, M = carryM;
+      for (int c = c0; c < c1; ++c) {
+        const unsigned int R = ch.m[kMR][c], H = ch.m[kMH][c];
+        ch.c[kCA][c] = Ar;
+        ch.c[kCB][c] = Br;
+        ch.c[kCP][c] = Pr;
+        ch.c[kCM][c] = M;
+        if (H) M = Pr + __popc(R & lowmask(31 - __clz(H)));
+        const int pr = __popc(R);
+        Pr += pr;
+        Ar += pr + __popc(ch.m[kMU][c]);
+        Br += __popc(ch.m[kMT][c]);
+      }
+      int N = carryN;
+      for (int c = c1 - 1; c >= c0; --c) {
+        ch.c[kCN][c] = N;
+        const unsigned int H = ch.m[kMH][c];
+        if (H) N = ch.c[kCP][c] + __popc(ch.m[kMR][c] & lowmask(__ffs(H) - 1));
+      }
     }
     gsync<G>();
     TCCD_PHASE(5);
@@ -892,13 +857,32 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     // are deferred, K = the largest k with
     //   sum_{r<k} children_r + sum_{r>=k} boxes_r <= cap
     // (at least one query advances: if none fits, the first is evicted).
-    for (int s = tid; s < Q; s += NT) {
-      int t = 0;
-      if (S.cont[s]) {
-        t = (S.segA1[s] - S.segA0[s]) + (S.segB1[s] - S.segB0[s]);
-        if (t > qcap) evict(s, t);
+    // Segment bounds of the flat prefixes, O(1) each from the chunk masks.
+    {
+      const int A_tot = S.A_tot, B_tot = S.B_tot, P_tot = S.P_tot;
+      auto prefix = [&](int x, int& pa, int& pb, int& pp) {
+        if (x >= n) { pa = A_tot; pb = B_tot; pp = P_tot; return; }
+        const int c = x >> 5;
+        const unsigned int lm = lowmask(x & 31);
+        const int pr = __popc(ch.m[kMR][c] & lm);
+        pa = ch.c[kCA][c] + pr + __popc(ch.m[kMU][c] & lm);
+        pb = ch.c[kCB][c] + __popc(ch.m[kMT][c] & lm);
+        pp = ch.c[kCP][c] + pr;
+      };
+      for (int s = tid; s < Q; s += NT) {
+        int t = 0;
+        if (S.cont[s]) {
+          int a0, b0, p0, a1, b1, p1;
+          prefix(S.seg_off[s], a0, b0, p0);
+          prefix(S.seg_off[s] + S.seg_n[s], a1, b1, p1);
+          S.segA0[s] = a0; S.segB0[s] = b0; S.segP0[s] = p0;
+          S.segA1[s] = a1; S.segB1[s] = b1; S.segP1[s] = p1;
+          t = (a1 - a0) + (b1 - b0);
+          if (!S.uniform[s]) S.any_general = 1;
+          if (t > qcap) evict(s, t);
+        }
+        S.tot[s] = t;
       }
-      S.tot[s] = t;
     }
     gsync<G>();
     TCCD_PHASE(6);
@@ -1003,104 +987,94 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     // t_lo order (push order).  t split: within a run of equal t_lo, all
     // lower children (t_lo kept) then all upper children (t_lo + w/2, below
     // the next run's t_lo), so with P = refining boxes before the parent,
-    // M / N = P at the run's head / at the next head:
+    // M / N = P at the run's head / at the next head (or the segment end):
     //   rank(lower) = M + P,  rank(upper) = N + P   (segment-relative).
     // New run heads: the children of the first refining box of a run.
+    // Lane per box; P, M, N and A from the chunk masks in O(1).
     const int nxt = prv;
     {
-      int Pr = P_end, Ar = A_end, N = carryN;
       unsigned int* const outr = ar.ref[nxt];
       uint8_t* const sln = slot_of[nxt];
       uint8_t* const fln = flags[nxt];
-      ByteVecReader<!Cfg::SMEM> rsl(sl), rfl(fl);
-      OffVecReader<!Cfg::SMEM, Off> roffA(offA);
-      int cslot = -1, cs = 0, c_off = 0, c_next = 0, c_S0 = 0, c_A0 = 0;
-      bool c_uni = false, c_hand = false;
-      for (int i = hi4 - 1; i >= lo4; --i) {
-        const int s = rsl(i);
-        if (s == kPNone) continue;
-        if (s != cslot) {
-          cslot = s;
-          cs = S.cont[s];
-          c_off = S.seg_off[s];
-          c_next = S.next_off[s];
-          c_S0 = S.segP0[s];
-          c_A0 = S.segA0[s];
-          c_uni = S.uniform[s] != 0;
-          c_hand = cs == 3 && S.hoff[s] >= 0;
-        }
-        const uint8_t f = rfl(i);
-        const int k = i - c_off;
+      for (int i = tid; i < n; i += NT) {
+        const int s = sl[i];
+        const int cs = S.cont[s];
+        if (cs == 0) continue;
+        const uint8_t f = fl[i];
         if (cs == 2) {
-          const int pos = c_next + k;
+          const int pos = S.next_off[s] + (i - S.seg_off[s]);
           outr[pos] = (unsigned)i | kRefSelf;
           sln[pos] = (uint8_t)s;
           fln[pos] = f;
+          continue;
         }
-        if (cs != 0 && (f & 3) != kDisjoint && !(f & 4)) {
-          const int sdim = (f >> 3) & 3;
-          Pr -= 1;
-          Ar -= 1 + ((sdim != 0 && (f & 32)) ? 1 : 0);
-          const bool hand = c_hand;
-          if ((cs == 1 || hand) && c_uni) {
-            const int M = roffA(i);
-            const int S0 = c_S0;
-            const uint8_t hd = Pr == M ? kHead : 0;
-            int rl, ru = -1;
-            if (sdim == 0) {
-              rl = (M - S0) + (Pr - S0);
-              ru = (N - S0) + (Pr - S0);
-            } else {
-              rl = Ar - c_A0;
-              if (f & 32) ru = rl + 1;
-            }
-            const uint8_t hu = sdim == 0 ? hd : 0;
-            if (!hand) {
-              const int base = c_next;
-              outr[base + rl] = (unsigned)i;
-              sln[base + rl] = (uint8_t)s;
-              fln[base + rl] = hd;
-              if (ru >= 0) {
-                outr[base + ru] = (unsigned)i | kRefCb;
-                sln[base + ru] = (uint8_t)s;
-                fln[base + ru] = hu;
-              }
-            } else {
-              // materialize the handed-over level in the next tier's pool
-              const long long base = S.hoff[s];
-              const Box pb = bx[i];
-              double mid;
-              const int sd = split_dim(pb, S.qp[s].kap, mid);
-              Box c0, c1;
-              children(pb, sd, mid, c0, c1);
-              io.out_pbox[base + rl] = c0;
-              io.out_pflag[base + rl] = hd;
-              if (ru >= 0) {
-                io.out_pbox[base + ru] = c1;
-                io.out_pflag[base + ru] = hu;
-              }
-            }
+        if ((f & 3) == kDisjoint || (f & 4) || !S.uniform[s]) continue;
+        const bool hand = cs == 3 && S.hoff[s] >= 0;
+        if (cs != 1 && !hand) continue;
+        const int c = i >> 5, l = i & 31;
+        const unsigned int lm = lowmask(l), bit = 1u << l;
+        const unsigned int R = ch.m[kMR][c], H = ch.m[kMH][c];
+        const int cP = ch.c[kCP][c];
+        const int Pr = cP + __popc(R & lm);
+        const unsigned int hle = H & (lm | bit), hgt = H & ~(lm | bit);
+        const int M = hle ? cP + __popc(R & lowmask(31 - __clz(hle))) : ch.c[kCM][c];
+        int N = hgt ? cP + __popc(R & lowmask(__ffs(hgt) - 1)) : ch.c[kCN][c];
+        if (N > S.segP1[s]) N = S.segP1[s];  // the last run ends at the segment end
+        const int S0 = S.segP0[s];
+        const int sdim = (f >> 3) & 3;
+        const uint8_t hd = Pr == M ? kHead : 0;
+        int rl, ru = -1;
+        if (sdim == 0) {
+          rl = (M - S0) + (Pr - S0);
+          ru = (N - S0) + (Pr - S0);
+        } else {
+          rl = ch.c[kCA][c] + __popc(R & lm) + __popc(ch.m[kMU][c] & lm) - S.segA0[s];
+          if (f & 32) ru = rl + 1;
+        }
+        const uint8_t hu = sdim == 0 ? hd : 0;
+        if (!hand) {
+          const int base = S.next_off[s];
+          outr[base + rl] = (unsigned)i;
+          sln[base + rl] = (uint8_t)s;
+          fln[base + rl] = hd;
+          if (ru >= 0) {
+            outr[base + ru] = (unsigned)i | kRefCb;
+            sln[base + ru] = (uint8_t)s;
+            fln[base + ru] = hu;
+          }
+        } else {
+          // materialize the handed-over level in the next tier's pool
+          const long long base = S.hoff[s];
+          const Box pb = bx[i];
+          double mid;
+          const int sd = split_dim(pb, S.qp[s].kap, mid);
+          Box c0, c1;
+          children(pb, sd, mid, c0, c1);
+          io.out_pbox[base + rl] = c0;
+          io.out_pflag[base + rl] = hd;
+          if (ru >= 0) {
+            io.out_pbox[base + ru] = c1;
+            io.out_pflag[base + ru] = hu;
           }
         }
-        if (f & kHead) N = Pr;
       }
     }
     gsync<G>();
     TCCD_PHASE(8);
     if (S.any_general) {
-    // ================= P5b: A / B entries (key, push, ref); deferred carry-over
+    // ================= P5b: A / B entries (key, push, ref)
+    // Entries are written for every refining box of the list (whatever its
+    // query's state) so that no stale entry sits inside the flat A / B ranges.
     for (int i = tid; i < n; i += NT) {
-      const int s = sl[i];
-      if (s == kPNone) continue;
-      const int k = i - S.seg_off[s];
-      // entries are written for every query counted in P4 (kept, deferred or
-      // evicted) so that no stale entry sits inside the flat A / B ranges
-      if (S.cont[s] == 0) continue;
       const uint8_t f = fl[i];
       if ((f & 3) == kDisjoint || (f & 4)) continue;
       const int sdim = (f >> 3) & 3;
       const Box b = bx[i];
-      const unsigned int oa = offA[i], ob = offB[i];
+      const int c = i >> 5;
+      const unsigned int lm = lowmask(i & 31);
+      const unsigned int oa = (unsigned)(ch.c[kCA][c] + __popc(ch.m[kMR][c] & lm) +
+                                         __popc(ch.m[kMU][c] & lm));
+      const unsigned int ob = (unsigned)(ch.c[kCB][c] + __popc(ch.m[kMT][c] & lm));
       const unsigned int push = oa + ob;
       const unsigned long long k0 = tkey(b.t0);
       ar.akey[oa] = k0;

@@ -84,6 +84,19 @@ def test_workload_samples_vs_oracle(cuda, config, start, count, kw):
     _vs_oracle(w, cuda, sep=kw.get("sep"), t_max=kw.get("t_max"))
 
 
+@pytest.mark.parametrize("config,start,count", [(0, 3_000, 20_000), (1, 70_000, 20_000),
+                                                (2, 12_000, 1_500)])
+def test_mixed_dyadic_and_general_t_max(cuda, config, start, count):
+    """Per-query t_max mixing powers of two (closed-form order) and other
+    values (general merge order) in one batch, so segments of both kinds sit
+    next to each other in every level list."""
+    from paper_2009_13349_b200 import workloads as W
+    w = W.generate(config, start, count)
+    rng = np.random.default_rng(config + 77)
+    t_max = rng.choice(np.array([1.0, 0.5, 0.25, 0.3, 0.7, 0.9]), count)
+    _vs_oracle(w, cuda, t_max=t_max)
+
+
 def test_extreme_coordinates_nan_path(cuda):
     """Coordinates near the top of the binary64 range: lerps and corner values
     overflow to +-inf and inf - inf = NaN.  The reference's hull ignores NaN
