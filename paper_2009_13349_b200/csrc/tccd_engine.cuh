@@ -239,6 +239,12 @@ constexpr int kCA = 0, kCB = 1, kCP = 2, kCM = 3, kCN = 4;
 
 __device__ __forceinline__ unsigned int lowmask(int k) { return (1u << k) - 1u; }  // k < 32
 
+// a[k] of a two-entry pointer array as a select: dynamic indexing would put
+// the array in local memory and turn shared-memory accesses through the
+// pointer into generic ones
+template <class T>
+__device__ __forceinline__ T* pick(T* const (&a)[2], int k) { return k ? a[1] : a[0]; }
+
 // global arena of one group
 template <class Cfg>
 struct EngineArena {
@@ -601,15 +607,15 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       if (tid == 0) { S.seg_off[s] = pos; S.seg_n[s] = nr; }
       if (off < 0) {
         if (tid == 0) {
-          ar.ref[cur][pos] = kRefRoot;
-          slot_of[cur][pos] = (uint8_t)s;
-          flags[cur][pos] = S.root_flag[s] | kHead;
+          pick(ar.ref, cur)[pos] = kRefRoot;
+          pick(slot_of, cur)[pos] = (uint8_t)s;
+          pick(flags, cur)[pos] = S.root_flag[s] | kHead;
         }
       } else {
         for (int b = tid; b < nr; b += NT) {
-          ar.ref[cur][pos + b] = kRefExt | (unsigned)(off + b);
-          slot_of[cur][pos + b] = (uint8_t)s;
-          flags[cur][pos + b] = io.in_pflag[off + b];
+          pick(ar.ref, cur)[pos + b] = kRefExt | (unsigned)(off + b);
+          pick(slot_of, cur)[pos + b] = (uint8_t)s;
+          pick(flags, cur)[pos + b] = io.in_pflag[off + b];
         }
       }
     }
@@ -629,13 +635,13 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     if (n == 0) break;
     ++rounds;
     boxes += (unsigned long long)n;
-    Box* const bx = ar.box[cur];
-    const Box* const bprev = ar.box[prv];
-    double* const wbc = ar.wb[cur];
-    const double* const wbp = ar.wb[prv];
-    const unsigned int* const rf = ar.ref[cur];
-    uint8_t* const sl = slot_of[cur];
-    uint8_t* const fl = flags[cur];
+    Box* const bx = pick(ar.box, cur);
+    const Box* const bprev = pick(ar.box, prv);
+    double* const wbc = pick(ar.wb, cur);
+    const double* const wbp = pick(ar.wb, prv);
+    const unsigned int* const rf = pick(ar.ref, cur);
+    uint8_t* const sl = pick(slot_of, cur);
+    uint8_t* const fl = pick(flags, cur);
     // ================= P1: materialize + classify
     // software pipeline: the reference of box i + 2*NT and the parent box of
     // box i + NT are in flight while box i is classified
@@ -993,9 +999,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     // Lane per box; P, M, N and A from the chunk masks in O(1).
     const int nxt = prv;
     {
-      unsigned int* const outr = ar.ref[nxt];
-      uint8_t* const sln = slot_of[nxt];
-      uint8_t* const fln = flags[nxt];
+      unsigned int* const outr = pick(ar.ref, nxt);
+      uint8_t* const sln = pick(slot_of, nxt);
+      uint8_t* const fln = pick(flags, nxt);
       for (int i = tid; i < n; i += NT) {
         const int s = sl[i];
         const int cs = S.cont[s];
@@ -1108,9 +1114,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     // ================= P6: merge by rank into the next level's reference list
     {
       const int A_tot = S.A_tot, B_tot = S.B_tot;
-      unsigned int* out = ar.ref[nxt];
-      uint8_t* sln = slot_of[nxt];
-      uint8_t* fln = flags[nxt];
+      unsigned int* out = pick(ar.ref, nxt);
+      uint8_t* sln = pick(slot_of, nxt);
+      uint8_t* fln = pick(flags, nxt);
       for (int e = tid; e < A_tot + B_tot; e += NT) {
         const bool isA = e < A_tot;
         const int x = isA ? e : e - A_tot;
