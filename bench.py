@@ -13,11 +13,15 @@ value  = device-timed throughput, inputs resident in HBM, CUDA events on the
          launching stream, barrier + synchronize on both sides, max over ranks.
 e2e    = the same through the public API with pinned HOST inputs: H2D of
          points + kind and D2H of status + toi inside the timed region.
-roofline = algorithmic FP64 flops (per query P_kind + checks *
-         F_kind, F_VF = 200, F_EE = 174, P_VF = 248, P_EE = 222, checks = the
-         reference's own count, which the kernel reproduces exactly) / the
-         solve's average duration, vs the DFMA peak measured on this box by
-         libtccd_probe.so (FMA-counted; an FMA-free kernel is capped at 0.5).
+roofline = the dominant kernel (the light-tier engine_kernel): its
+         algorithmic FP64 flops per launch (F_VF = 200 / F_EE = 174
+         per box classification, counted per tier and kind by the library) /
+         its average duration, timed with CUDA events the library records on
+         the launching stream after every stage of every timed step; peak =
+         the DFMA rate measured on this box by libtccd_probe.so (FMA-counted;
+         an FMA-free kernel is capped at 0.5 of it).  traffic = that kernel's
+         DRAM bytes per launch from the committed ncu capture
+         (profiles/r01/roofline_traffic.json).
 cpu_baseline = the C restatement of the reference (oracle/, kind "port") on
          all host cores, rank 0 at N=1, on a bounded sample.
 --impl reference: that CPU path alone, same metric/config (rank 0 only).
@@ -193,7 +197,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_2009_13349_b200 import solve_batch
+    from paper_2009_13349_b200 import solve_batch, solver
     from paper_2009_13349_b200 import workloads as W
 
     torch.cuda.set_device(local)
@@ -223,9 +227,9 @@ def main():
         kw = dict(delta=torch.from_numpy(w.delta).to(dev), max_checks=torch.from_numpy(w.max_checks).to(dev))
     stream = torch.cuda.current_stream(dev)
 
-    def step():
+    def step(events=None):
         return solve_batch(pts, kind, outputs=("status", "toi"), device=dev,
-                           raise_on_error=False, **kw)
+                           raise_on_error=False, events=events, **kw)
 
     # untimed: full outputs once, for the algorithmic work (checks) and hits
     full = solve_batch(pts, kind, device=dev, stats=True, **kw)
@@ -244,23 +248,41 @@ def main():
     barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # per step: solve start + the library's 4 stage events (prologue, light,
+    # medium, giant done), all on the launching stream; handles created here
+    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for row in sev:
+        for ev in row:
+            ev.record(stream)
+    torch.cuda.synchronize(dev)
     e0.record(stream)
-    for _ in range(args.steps):
-        step()
+    for k in range(args.steps):
+        sev[k][0].record(stream)
+        step(sev[k][1:])
     e1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    stage_names = ("prologue", "light", "medium", "giant")
+    stage_ms = {nm: statistics.mean(sev[k][j].elapsed_time(sev[k][j + 1]) for k in range(args.steps))
+                for j, nm in enumerate(stage_names)}
     # end to end through the public API with pinned host buffers
     barrier()
     torch.cuda.synchronize(dev)
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kw_h = {k: v.cpu() for k, v in kw.items()}
     f0.record(stream)
-    for _ in range(args.steps):
-        r = solve_batch(pts_h, kind_h, outputs=("status", "toi"), device=dev,
-                        raise_on_error=False, **({k: v.cpu() for k, v in kw.items()}))
-    f1.record(stream)
+    # the points copies run on the API's side stream, ordered after f0; each
+    # solve waits for its copy, so step k+1's copy overlaps step k's solve
+    solver.copy_stream(dev).wait_event(f0)
+    t_wall = time.perf_counter()
+    res = [solve_batch(pts_h, kind_h, outputs=("status", "toi"), device=dev, non_blocking=True,
+                       **kw_h) for _ in range(args.steps)]
+    f1.record(stream)  # after the last results' D2H
     torch.cuda.synchronize(dev)
+    t_wall = time.perf_counter() - t_wall
+    e2e_hits = [int((r["status"] == 1).sum()) for r in res]
+    assert all(h == hits for h in e2e_hits), "e2e results differ from the device-input solve"
     barrier()
     clk = clocks.stop()
     e2e_ms = f0.elapsed_time(f1) / args.steps
@@ -277,7 +299,18 @@ def main():
         return
 
     peaks = fp64_peaks()
-    achieved = flops / (ms * 1e-3) / 1e12
+    st = [int(x) for x in full["stats"].tolist()]
+    tier_flops = {nm: st[8 + 2 * t] * F_CHECK[0] + st[9 + 2 * t] * F_CHECK[1]
+                  for t, nm in enumerate(("light", "medium", "giant"))}
+    dom = max(("light", "medium", "giant"), key=lambda nm: stage_ms[nm])
+    achieved = tier_flops[dom] / (stage_ms[dom] * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        if tj.get("kernel") == dom and tj.get("config") == args.config and tj.get("queries") == Q:
+            traffic = tj["dram_bytes_per_launch"]
     cpu = None
     if world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
@@ -293,15 +326,26 @@ def main():
         "config": workload_desc(args.config, Q),
         "e2e": {"value": e2e_value, "unit": "queries/s",
                 "h2d_bytes_per_step": int(pts_h.numel() * 8 + kind_h.numel()),
-                "d2h_bytes_per_step": int(Q * 9)},
+                "d2h_bytes_per_step": int(Q * 9),
+                "api": "solve_batch(pinned host points/kind, non_blocking=True): points H2D on "
+                       "the API's copy stream (overlaps the previous step's solve), status+toi "
+                       "D2H into pinned host tensors; CUDA events on the launching stream",
+                "wall_ms_per_step": 1e3 * t_wall / args.steps},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peaks["dfma_tflops"],
                      "unit": "TFLOP/s", "frac": achieved / peaks["dfma_tflops"],
-                     "traffic": None,
+                     "traffic": traffic,
+                     "kernel": f"engine_kernel ({dom} tier)",
+                     "kernel_flops_per_launch": tier_flops[dom],
+                     "kernel_ms": stage_ms[dom],
+                     "share_of_step": stage_ms[dom] / ms,
+                     "stage_ms": stage_ms,
                      "peak_source": "measured on this box: DFMA probe (libtccd_probe.so), FMA-counted",
                      "fma_free_ceiling_tflops": peaks["dadd_tflops"],
-                     "flops_per_step": flops,
-                     "kernels": "one solve = prologue_kernel + engine_kernel x3 tiers "
-                                 "(light / medium / giant), CUDA events on the launching stream"},
+                     "frac_of_fma_free_ceiling": achieved / peaks["dadd_tflops"],
+                     "solve_flops_per_step": flops,
+                     "solve_achieved_tflops": flops / (ms * 1e-3) / 1e12,
+                     "traffic_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum"
+                                       " (profiles/r01/roofline_traffic.json)"},
         "cpu_baseline": cpu,
         "clocks": clk,
         "gpu_launches": 2 * args.steps * LAUNCHES_PER_SOLVE * ((Q + (1 << 22) - 1) >> 22),
@@ -309,7 +353,8 @@ def main():
                            "max_checks": int(checks.max()), "giant_tier_queries": evicted,
                            "engine_rounds": pool_rounds, "level_deferrals": deferrals,
                            "medium_tier_queries": int(full["stats"][3].item()),
-                           "boxes_per_tier": [int(x) for x in full["stats"][4:7].tolist()]},
+                           "boxes_per_tier": st[4:7],
+                           "classifications_per_tier_vf_ee": [st[8:10], st[10:12], st[12:14]]},
     }
     print(json.dumps(line), flush=True)
     if world > 1:

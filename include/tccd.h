@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TCCD_ABI_VERSION 1
+#define TCCD_ABI_VERSION 2
 
 /* Per-query status values written to tccd_batch.status. */
 #define TCCD_STATUS_FREE 0           /* certified collision free, toi = +inf   */
@@ -114,11 +114,19 @@ typedef struct tccd_batch {
   size_t workspace_bytes;
   int32_t heavy_blocks; /* concurrent block-per-query solvers; 0 = default   */
   int32_t device_sms;   /* SM count of the target device; 0 = query it      */
-  int64_t *stats;       /* optional device [8] diagnostics: [0] queries
+  int64_t *stats;       /* optional device [16] diagnostics: [0] queries
                            that reached the giant tier, [1] engine rounds,
                            [2] level deferrals, [3] queries that reached the
                            medium tier, [4..6] boxes visited per tier
-                           (light, medium, giant), [7] reserved           */
+                           (light, medium, giant), [7] reserved, [8..13]
+                           box classifications per tier and kind (light
+                           VF, light EE, medium VF, medium EE, giant VF,
+                           giant EE), [14..15] reserved                  */
+  void *const *events;  /* optional host array of 4 cudaEvent_t (NULL
+                           entries skipped), recorded on `stream` after the
+                           prologue, light, medium and giant stages of each
+                           4M-query chunk: per-kernel timing on the
+                           launching stream (ABI 2)                       */
 } tccd_batch;
 
 /* Bytes of device workspace tccd_solve_batch needs for a batch of n queries

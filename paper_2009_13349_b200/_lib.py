@@ -13,7 +13,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TCCD_LIB") or os.path.join(_HERE, "libtccd.so")  # override: experiments only
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 FLAG_HEAVY_ONLY = 1
 
 STATUS_FREE = 0
@@ -59,6 +59,7 @@ class TccdBatch(ctypes.Structure):
         ("heavy_blocks", ctypes.c_int32),
         ("device_sms", ctypes.c_int32),
         ("stats", _vp),
+        ("events", _vp),
     ]
 
 

@@ -41,6 +41,7 @@ struct Counters {
   unsigned long long boxes[3];    // boxes handled per tier (diagnostics)
   unsigned long long pool[3];     // handover pool fill (tiers 1, 2)
   unsigned long long phase[3][16];  // cycles per engine phase (TCCD_PHASE_PROF builds)
+  unsigned long long cls[3][2];   // box classifications per tier and kind (VF, EE)
 };
 
 // A queued query, self-contained so a tier admits it with one coalesced
@@ -312,6 +313,7 @@ __global__ void stats_kernel(Args a, int heavy_only) {
     a.stats[2] += (long long)a.ctr->deferred;
     a.stats[3] += (long long)a.ctr->evicted[0];
     for (int k = 0; k < 3; ++k) a.stats[4 + k] += (long long)a.ctr->boxes[k];
+    for (int k = 0; k < 6; ++k) a.stats[8 + k] += (long long)a.ctr->cls[k / 2][k % 2];
   }
 }
 
@@ -493,13 +495,18 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
     io.evicted = &a.ctr->evicted[tier];
     io.boxes = &a.ctr->boxes[tier];
     io.phase = a.ctr->phase[tier];
+    io.cls = a.ctr->cls[tier];
     if (tier == 0) { io.arenas = ws + L.light; io.arena_bytes = L.light_b; io.cap = LightCfg::CAP; }
     if (tier == 1) { io.arenas = ws + L.medium; io.arena_bytes = L.medium_b; io.cap = MediumCfg::CAP; }
     if (tier == 2) { io.arenas = ws + L.giant; io.arena_bytes = L.giant_b; io.cap = giant_cap(mcmax); }
     return io;
   };
 
-  if (a.stats && cudaMemsetAsync(a.stats, 0, 8 * sizeof(long long), st) != cudaSuccess)
+  // optional caller events, recorded after each stage of every chunk
+  auto mark = [&](int k) {
+    return b->events && b->events[k] ? cudaEventRecord((cudaEvent_t)b->events[k], st) : cudaSuccess;
+  };
+  if (a.stats && cudaMemsetAsync(a.stats, 0, 16 * sizeof(long long), st) != cudaSuccess)
     return TCCD_E_CUDA;
   for (long long lo = 0; lo < b->n; lo += kChunk) {
     const long long cnt = b->n - lo < kChunk ? b->n - lo : kChunk;
@@ -512,13 +519,18 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
     const unsigned pblocks = (unsigned)((cnt + kPrologueThreads - 1) / kPrologueThreads);
     prologue_kernel<<<pblocks, kPrologueThreads, 0, st>>>(a, lo, cnt, queue[first],
                                                          &a.ctr->q_count[first]);
-    if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
+    if (cudaGetLastError() != cudaSuccess || mark(0) != cudaSuccess) return TCCD_E_CUDA;
     int rc;
     if (!a.heavy_only) {
       if ((rc = launch_tier<LightCfg>(a, io_for(0), L.light_blocks, st)) != TCCD_OK) return rc;
+      if (mark(1) != cudaSuccess) return TCCD_E_CUDA;
       if ((rc = launch_tier<MediumCfg>(a, io_for(1), L.medium_blocks, st)) != TCCD_OK) return rc;
+      if (mark(2) != cudaSuccess) return TCCD_E_CUDA;
+    } else if (mark(1) != cudaSuccess || mark(2) != cudaSuccess) {
+      return TCCD_E_CUDA;
     }
     if ((rc = launch_tier<GiantCfg>(a, io_for(2), L.giant_blocks, st)) != TCCD_OK) return rc;
+    if (mark(3) != cudaSuccess) return TCCD_E_CUDA;
     if (a.stats) {
       stats_kernel<<<1, 32, 0, st>>>(a, a.heavy_only);
       if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;

@@ -397,6 +397,7 @@ struct TierIO {
   unsigned long long* evicted;
   unsigned long long* boxes;
   unsigned long long* phase;  // [16] cycles per phase (TCCD_PHASE_PROF builds)
+  unsigned long long* cls;    // [2] box classifications (VF, EE)
 };
 
 template <class Cfg>
@@ -438,6 +439,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   int cur = 0;
   long long rounds = 0;
   unsigned long long evicted = 0, boxes = 0;
+  unsigned int ncls_vf = 0, ncls_ee = 0;  // this thread's classifications per kind
 #ifdef TCCD_PHASE_PROF
   unsigned long long ph_acc[16] = {0};
   long long ph_last = clock64();
@@ -688,13 +690,14 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           b = (r & kRefCb) ? c1 : c0;
         }
       }
-      bx[i] = b;
       const int k = i - S.seg_off[s];
       if (!(f & kClassified)) {
         const long long cut = qp.max_checks - S.C[s] - 1;
         if (k <= cut) {
           const uint8_t head = f & kHead;
           const int cls = classify((const double*)S.P[s], qp.kind, b, qp.eps, qp.sep, wb, qp.tame != 0);
+          ncls_ee += qp.kind;  // (kind is 0 or 1)
+          ncls_vf += 1 - qp.kind;
           f = (uint8_t)cls;
           if (cls != kDisjoint) {
             int sdim; double mid; bool ph;
@@ -705,6 +708,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         }
       }
       if ((f & 3) != kDisjoint) {
+        // only non-disjoint boxes are read again (parents, first / drop
+        // records, merge keys): disjoint ones are never stored, which keeps
+        // the level arrays' footprint in L2
+        bx[i] = b;
         wbc[i] = wb;
         atomicMin(&S.j[s], k);
         // first accepted box: if it is not j itself it lies after j, and it is
@@ -1204,6 +1211,12 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
 #endif
   }
   if (evicted) atomicAdd(io.evicted, evicted);
+  {  // (all lanes reach here: the round loop exits group-wide)
+    const unsigned int wv = __reduce_add_sync(0xffffffffu, ncls_vf);
+    const unsigned int we = __reduce_add_sync(0xffffffffu, ncls_ee);
+    if (lane == 0 && wv) atomicAdd(&io.cls[0], (unsigned long long)wv);
+    if (lane == 0 && we) atomicAdd(&io.cls[1], (unsigned long long)we);
+  }
 }
 
 }  // namespace tccd

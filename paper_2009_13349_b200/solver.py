@@ -23,6 +23,17 @@ from .inclusion import FilterEps
 OUTPUT_FIELDS = ("status", "toi", "tol", "codom", "checks", "early", "witness", "level")
 
 _workspaces: dict = {}
+_copy_streams: dict = {}
+
+
+def copy_stream(device: torch.device) -> torch.cuda.Stream:
+    """The per-device side stream host-input points are copied on when
+    ``solve_batch(..., non_blocking=True)``."""
+    key = (device.type, device.index)
+    cs = _copy_streams.get(key)
+    if cs is None:
+        cs = _copy_streams[key] = torch.cuda.Stream(device)
+    return cs
 
 
 def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
@@ -37,6 +48,7 @@ def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
 
 def release_workspaces() -> None:
     _workspaces.clear()
+    _heavy_blocks_cache.clear()
 
 
 def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -48,9 +60,24 @@ def sm_count(device: torch.device) -> int:
     return torch.cuda.get_device_properties(device).multi_processor_count
 
 
+_heavy_blocks_cache: dict = {}
+
+
 def default_heavy_blocks(device: torch.device, n: int = 1, max_checks_max: int = 1) -> int:
     """Giant-tier CTAs: one per SM, fewer if their 2*m_I-box arenas would take
-    more than half of the free device memory."""
+    more than half of the free device memory.  Cached per (device, n,
+    max_checks_max): cudaMemGetInfo can stall the host for milliseconds while
+    the device is busy."""
+    key = (device.index, int(n), int(max_checks_max))
+    hb = _heavy_blocks_cache.get(key)
+    if hb is None:
+        if len(_heavy_blocks_cache) > 64:
+            _heavy_blocks_cache.clear()
+        hb = _heavy_blocks_cache[key] = _default_heavy_blocks(device, n, max_checks_max)
+    return hb
+
+
+def _default_heavy_blocks(device: torch.device, n: int, max_checks_max: int) -> int:
     sms = sm_count(device)
     lib = _lib.lib()
     base = int(lib.tccd_workspace_bytes(int(n), int(max_checks_max), 1))
@@ -87,7 +114,7 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
                 max_checks=None, separation=None, t_max=None, eps=None,
                 outputs=OUTPUT_FIELDS, device=None, heavy_only: bool = False,
                 heavy_blocks: int | None = None, raise_on_error: bool = True,
-                stats: bool = False) -> dict:
+                stats: bool = False, events=None, non_blocking: bool = False) -> dict:
     """Solve a batch of CCD queries on one GPU.
 
     points: [n, 8, 3] float64 (torch tensor or numpy), start block then end
@@ -102,6 +129,18 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
     back on the host; device inputs stay on their device.  Returns a dict of
     tensors keyed by ``outputs`` (subset of OUTPUT_FIELDS; status and toi are
     always present).
+
+    non_blocking=True (host inputs): the points are copied on a side stream
+    (``copy_stream``), so the copy of the next batch overlaps this batch's
+    solve; the results are copied back into pinned host tensors without a
+    host synchronization: they are valid once out["ready"] (a CUDA event on
+    the launching stream) has completed, and per-query errors are not
+    raised (check status after synchronizing).
+
+    stats=True adds out["stats"], the library's 16 diagnostic counters
+    (include/tccd.h).  events: optional 4 torch.cuda.Event(enable_timing=True),
+    recorded on the launching stream after the prologue, light, medium and
+    giant stages (per-kernel timing).
     """
     config = config or SolverConfig()
     host_in = not (isinstance(points, torch.Tensor) and points.is_cuda)
@@ -117,7 +156,15 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
     n = int(pts.shape[0])
     if host_in:
         pts = pts.contiguous().pin_memory() if pts.device.type == "cpu" else pts
-    pts = pts.to(dev, non_blocking=True).contiguous()
+    if host_in and non_blocking:
+        compute = torch.cuda.current_stream(dev)
+        cs = copy_stream(dev)
+        with torch.cuda.stream(cs):
+            pts = pts.to(dev, non_blocking=True).contiguous()
+        compute.wait_stream(cs)
+        pts.record_stream(compute)
+    else:
+        pts = pts.to(dev, non_blocking=True).contiguous()
 
     if isinstance(kind, (int, np.integer, QueryKind)):
         kind_t, kind_all = None, int(kind)
@@ -163,7 +210,15 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
     if "early" in want: out["early"] = torch.empty(n, dtype=torch.uint8, device=dev)
     if "witness" in want: out["witness"] = torch.empty((n, 6), dtype=torch.float64, device=dev)
     if "level" in want: out["level"] = torch.empty(n, dtype=torch.int32, device=dev)
-    st = torch.zeros(8, dtype=torch.int64, device=dev) if stats else None
+    st = torch.zeros(16, dtype=torch.int64, device=dev) if stats else None
+    ev_arr = None
+    if events is not None:
+        if len(events) != 4:
+            raise ValueError("events must hold 4 torch.cuda.Event")
+        for ev in events:
+            if ev.cuda_event == 0:  # torch creates the handle on first record
+                ev.record(torch.cuda.current_stream(dev))
+        ev_arr = (ctypes.c_void_p * 4)(*[ev.cuda_event for ev in events])
 
     with torch.cuda.device(dev):
         hb = heavy_blocks or default_heavy_blocks(dev, n, mc_max)
@@ -193,11 +248,19 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
         b.heavy_blocks = hb
         b.device_sms = sm_count(dev)
         b.stats = _ptr(st)
+        b.events = ctypes.cast(ev_arr, ctypes.c_void_p) if ev_arr is not None else None
         stream = torch.cuda.current_stream(dev)
         rc = lib.tccd_solve_batch(ctypes.byref(b), ctypes.c_void_p(stream.cuda_stream))
         _raise_abi(rc, delta_all, mc_all, tm_all, sep_all, kind_all)
     if host_in:
         out = {k: v.to("cpu", non_blocking=True) for k, v in out.items()}
+        if non_blocking:
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream(dev))
+            out["ready"] = ready
+            if st is not None:
+                out["stats"] = st
+            return out
         torch.cuda.current_stream(dev).synchronize()
     if st is not None:
         out["stats"] = st

@@ -300,3 +300,21 @@ def test_cli_run_and_fn_guard(cuda, tmp_path):
     bad = tmp_path / "bad.csv"
     bad.write_text(("0,1,0,1,10,1,1\n" + "0,1,0,1,0,1,1\n" + "1,1,0,1,0,1,1\n" + "0,1,1,1,0,1,1\n") * 2)
     assert cli.main(["run", "--dataset", str(bad), "--kind", "vf", "--format", "csv"]) == 2
+
+
+def test_non_blocking_host_pipeline(cuda):
+    """Back-to-back host-input solves with non_blocking=True (points copied on
+    the side stream while the previous batch solves) give the blocking
+    results once their ready events complete."""
+    from paper_2009_13349_b200 import solve_batch
+    from paper_2009_13349_b200 import workloads as W
+    ws = [W.generate(1, 200_000 + 30_000 * k, 30_000) for k in range(3)]
+    want = [solve_batch(torch.from_numpy(w.points), torch.from_numpy(w.kind), device=cuda)
+            for w in ws]
+    pinned = [(torch.from_numpy(w.points).pin_memory(), torch.from_numpy(w.kind).pin_memory())
+              for w in ws]
+    got = [solve_batch(p, k, device=cuda, non_blocking=True) for p, k in pinned]
+    for g, r in zip(got, want):
+        g["ready"].synchronize()
+        for key in ("status", "toi", "checks", "witness", "level"):
+            assert torch.equal(g[key], r[key]), key

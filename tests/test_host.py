@@ -184,7 +184,7 @@ def test_library_exports_every_header_symbol():
     assert set(syms) == set(_lib.EXPORTS)
     for name in syms:
         assert hasattr(L, name), name
-    assert L.tccd_abi_version() == 1
+    assert L.tccd_abi_version() == _lib.ABI_VERSION == 2
     for code in range(0, 12):
         assert L.tccd_error_string(code)
     assert b"unknown" in L.tccd_error_string(999)
