@@ -147,6 +147,39 @@ int tccd_solve_kernel(const double *s, const double *e, int kind, double t_max,
                       double delta, int64_t max_checks, double sep, double ex,
                       double ey, double ez, double *out13);
 
+/*
+ * GPU broad phase <- ccdkit.scene.broad_phase
+ * (pkg/src/ccdkit/scene.py:225-300): the primitive pairs whose inflated
+ * swept boxes overlap, minus pairs sharing a mesh vertex; vertex-face pairs
+ * (vertex, triangle) sorted, then edge-edge pairs (edge_a < edge_b) sorted,
+ * with their queries in the solver's [m][8][3] layout.
+ *
+ * Mesh arrays are DEVICE pointers; positions must be finite and indices in
+ * [0, n_vertices) (the Python layer validates, like TriMeshPair).  Edges
+ * are rows (i, j), i < j, unique (edges_from_triangles).
+ */
+typedef struct tccd_mesh {
+  uint32_t struct_size; /* = sizeof(tccd_mesh) */
+  uint32_t reserved;
+  int64_t n_vertices, n_triangles, n_edges;
+  const double *x0;          /* [n_vertices][3] positions at the step start */
+  const double *x1;          /* [n_vertices][3] positions at the step end   */
+  const int64_t *triangles;  /* [n_triangles][3]                            */
+  const int64_t *edges;      /* [n_edges][2]                                */
+} tccd_mesh;
+
+typedef struct tccd_broad tccd_broad; /* opaque broad-phase state */
+
+/* Boxes, grid and pair counts (stream-ordered device allocations owned by
+ * the handle).  Synchronizes `stream` and returns the candidate counts. */
+int tccd_broad_create(const tccd_mesh *mesh, double inflation, tccd_broad **out,
+                      int64_t *n_vf, int64_t *n_ee, void *stream);
+/* Writes the n_vf + n_ee candidates (VF block first) on the handle's
+ * stream: kind [m] u8, pairs [m][2] i64 (vertex, triangle) / (edge_a,
+ * edge_b), points [m][8][3] f64 (device buffers of the caller). */
+int tccd_broad_emit(tccd_broad *h, uint8_t *kind, int64_t *pairs, double *points);
+void tccd_broad_destroy(tccd_broad *h);
+
 const char *tccd_error_string(int code);
 int tccd_abi_version(void);
 

@@ -63,12 +63,31 @@ class TccdBatch(ctypes.Structure):
     ]
 
 
+class TccdMesh(ctypes.Structure):
+    """Mirror of ``struct tccd_mesh`` (include/tccd.h)."""
+
+    _fields_ = [
+        ("struct_size", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
+        ("n_vertices", ctypes.c_int64),
+        ("n_triangles", ctypes.c_int64),
+        ("n_edges", ctypes.c_int64),
+        ("x0", _vp),
+        ("x1", _vp),
+        ("triangles", _vp),
+        ("edges", _vp),
+    ]
+
+
 EXPORTS = (
     "tccd_abi_version",
     "tccd_error_string",
     "tccd_workspace_bytes",
     "tccd_solve_batch",
     "tccd_solve_kernel",
+    "tccd_broad_create",
+    "tccd_broad_emit",
+    "tccd_broad_destroy",
 )
 
 _lib = None
@@ -100,6 +119,14 @@ def lib() -> ctypes.CDLL:
         L.tccd_solve_kernel.argtypes = [
             _vp, _vp, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int64,
             ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, _vp]
+        L.tccd_broad_create.restype = ctypes.c_int
+        L.tccd_broad_create.argtypes = [ctypes.POINTER(TccdMesh), ctypes.c_double,
+                                        ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int64),
+                                        ctypes.POINTER(ctypes.c_int64), _vp]
+        L.tccd_broad_emit.restype = ctypes.c_int
+        L.tccd_broad_emit.argtypes = [_vp, _vp, _vp, _vp]
+        L.tccd_broad_destroy.restype = None
+        L.tccd_broad_destroy.argtypes = [_vp]
         v = L.tccd_abi_version()
         if v != ABI_VERSION:
             raise RuntimeError(f"libtccd ABI {v} != expected {ABI_VERSION}")

@@ -16,7 +16,9 @@ candidate set, in its order, and the narrow phase runs as batched
   per candidate.  Non-dyadic t_max goes through the engine's general
   ordering path.
 
-The broad phase itself runs on the host (a GPU version is §8(f) row 2).
+The broad phase runs on the GPU too (§8(f) row 2, csrc/broad.cu): the
+candidates are written straight into the solver's device layout, so the
+narrow phase reads them without a host round trip.
 """
 
 from __future__ import annotations
@@ -25,9 +27,12 @@ import math
 from dataclasses import dataclass
 from typing import Callable
 
+import ctypes
+
 import numpy as np
 import torch
 
+from . import _lib
 from .core import DomainBox, Query, QueryKind, SolverConfig
 from .inclusion import compute_filters, compute_gamma
 from .solver import solve_batch
@@ -106,27 +111,28 @@ class CandidateSet:
     """Broad-phase output in batch layout, reference order (VF pairs sorted
     by (vertex, triangle), then EE pairs sorted by (edge_a, edge_b))."""
 
-    kind: np.ndarray     # [m] u8
-    indices: np.ndarray  # [m, 2] int64
-    points: np.ndarray   # [m, 8, 3] f64
+    kind: object     # [m] u8 (torch device tensor, or numpy)
+    indices: object  # [m, 2] int64
+    points: object   # [m, 8, 3] f64
 
     @property
     def m(self) -> int:
         return int(self.kind.shape[0])
 
+    def host(self) -> "CandidateSet":
+        """The same candidates as numpy arrays."""
+        return CandidateSet(_np(self.kind), _np(self.indices), _np(self.points))
+
     def candidate(self, i: int) -> ContactCandidate:
-        q = Query(QueryKind(int(self.kind[i])), tuple(map(tuple, self.points[i, :4])),
-                  tuple(map(tuple, self.points[i, 4:])))
-        return ContactCandidate(QueryKind(int(self.kind[i])),
-                                (int(self.indices[i, 0]), int(self.indices[i, 1])), q)
+        p = self.points[i].tolist()
+        k = QueryKind(int(self.kind[i]))
+        ij = self.indices[i].tolist()
+        return ContactCandidate(k, (int(ij[0]), int(ij[1])), Query(k, tuple(map(tuple, p[:4])),
+                                                                  tuple(map(tuple, p[4:]))))
 
     def to_list(self) -> list:
-        return [self.candidate(i) for i in range(self.m)]
-
-
-def _boxes(mesh: TriMeshPair, idx: np.ndarray, inflation: float):
-    pts = np.stack((mesh.x0[idx], mesh.x1[idx]))  # (2, m, k, 3), scene.py:195-200
-    return pts.min(axis=(0, 2)) - inflation, pts.max(axis=(0, 2)) + inflation
+        h = self.host()
+        return [h.candidate(i) for i in range(h.m)]
 
 
 def load_obj(path) -> tuple[np.ndarray, np.ndarray]:
@@ -156,89 +162,68 @@ def load_obj(path) -> tuple[np.ndarray, np.ndarray]:
     return v, f
 
 
-def _overlapping_pairs(alo, ahi, blo, bhi):
-    """All (a, b) whose closed boxes overlap on every axis.
-
-    Sweep on x: b sorted by lower x bound; for each a the window is the b
-    with blo_x <= ahi_x and blo_x >= alo_x - 2*max_width (a superset of
-    bhi_x >= alo_x), then the exact test on all three axes."""
-    if len(alo) == 0 or len(blo) == 0:
-        return np.zeros((0, 2), dtype=np.int64)
-    order = np.argsort(blo[:, 0], kind="stable")
-    bstart = blo[order, 0]
-    wmax = float(np.max(bhi[:, 0] - blo[:, 0]))
-    hi_i = np.searchsorted(bstart, ahi[:, 0], side="right")
-    lo_i = np.minimum(np.searchsorted(bstart, alo[:, 0] - 2.0 * wmax, side="left"), hi_i)
-    cnt = hi_i - lo_i
-    a_rep = np.repeat(np.arange(len(alo)), cnt)
-    start = np.repeat(lo_i - (np.cumsum(cnt) - cnt), cnt)
-    b_rep = order[np.arange(len(a_rep)) + start]
-    ok = np.ones(len(a_rep), dtype=bool)
-    for k in range(3):
-        ok &= (alo[a_rep, k] <= bhi[b_rep, k]) & (blo[b_rep, k] <= ahi[a_rep, k])
-    return np.stack([a_rep[ok], b_rep[ok]], 1).astype(np.int64)
+def _np(x):
+    return x.cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
 
 
-def broad_phase_batch(mesh: TriMeshPair, inflation: float = 0.0) -> CandidateSet:
-    """Exactly the pairs of the reference broad phase (scene.py:225-300):
-    primitives whose inflated swept boxes overlap, minus pairs that share a
-    mesh vertex.  (The reference's grid hash is a superset filter followed by
-    the same exact box test, so its result is this set.)"""
+def broad_phase_batch(mesh: TriMeshPair, inflation: float = 0.0, device=None) -> CandidateSet:
+    """The reference broad phase's candidates (scene.py:225-300), found on
+    the GPU (csrc/broad.cu, tccd_broad_*): exactly the pairs whose inflated
+    swept boxes overlap, minus pairs sharing a mesh vertex, VF pairs sorted
+    by (vertex, triangle) then EE pairs by (edge_a, edge_b).  The reference's
+    grid hash is a superset filter followed by the same exact box test, so
+    its result is this set.  Returns device tensors: kind [m] u8, indices
+    [m, 2] i64, points [m, 8, 3] f64 (the solver's layout)."""
     if not (inflation >= 0.0 and math.isfinite(inflation)):
         raise ValueError("inflation must be >= 0 and finite")
-    n = mesh.n_vertices
-    empty = CandidateSet(np.zeros(0, np.uint8), np.zeros((0, 2), np.int64),
-                         np.zeros((0, 8, 3)))
-    if n == 0:
-        return empty
-    vlo, vhi = _boxes(mesh, np.arange(n, dtype=np.intp)[:, None], inflation)
-    tris, edges = mesh.triangles, mesh.edges
-    kinds, idxs, pts = [], [], []
-    if len(tris):
-        tlo, thi = _boxes(mesh, tris, inflation)
-        pr = _overlapping_pairs(vlo, vhi, tlo, thi)
-        keep = ~np.any(tris[pr[:, 1]] == pr[:, 0:1], axis=1)
-        pr = pr[keep]
-        pr = pr[np.lexsort((pr[:, 1], pr[:, 0]))]
-        if len(pr):
-            v, t = pr[:, 0], tris[pr[:, 1]]
-            vid = np.stack([v, t[:, 0], t[:, 1], t[:, 2]], 1)
-            kinds.append(np.zeros(len(pr), np.uint8))
-            idxs.append(pr)
-            pts.append(np.concatenate([mesh.x0[vid], mesh.x1[vid]], 1))
-    if len(edges):
-        elo, ehi = _boxes(mesh, edges, inflation)
-        pr = _overlapping_pairs(elo, ehi, elo, ehi)
-        pr = pr[pr[:, 0] < pr[:, 1]]
-        a, b = edges[pr[:, 0]], edges[pr[:, 1]]
-        share = (a[:, 0] == b[:, 0]) | (a[:, 0] == b[:, 1]) | (a[:, 1] == b[:, 0]) | \
-            (a[:, 1] == b[:, 1])
-        pr = pr[~share]
-        pr = pr[np.lexsort((pr[:, 1], pr[:, 0]))]
-        if len(pr):
-            a, b = edges[pr[:, 0]], edges[pr[:, 1]]
-            vid = np.stack([a[:, 0], a[:, 1], b[:, 0], b[:, 1]], 1)
-            kinds.append(np.ones(len(pr), np.uint8))
-            idxs.append(pr)
-            pts.append(np.concatenate([mesh.x0[vid], mesh.x1[vid]], 1))
-    if not kinds:
-        return empty
-    return CandidateSet(np.concatenate(kinds), np.concatenate(idxs),
-                        np.ascontiguousarray(np.concatenate(pts)))
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise RuntimeError("the broad phase runs on the GPU (there is no CPU fallback)")
+    L = _lib.lib()
+    with torch.cuda.device(dev):
+        x0 = torch.from_numpy(mesh.x0).to(dev)
+        x1 = torch.from_numpy(mesh.x1).to(dev)
+        tris = torch.from_numpy(np.ascontiguousarray(mesh.triangles, dtype=np.int64)).to(dev)
+        edges = torch.from_numpy(np.ascontiguousarray(mesh.edges, dtype=np.int64)).to(dev)
+        m = _lib.TccdMesh()
+        m.struct_size = ctypes.sizeof(_lib.TccdMesh)
+        m.n_vertices, m.n_triangles, m.n_edges = mesh.n_vertices, len(mesh.triangles), len(mesh.edges)
+        m.x0, m.x1 = x0.data_ptr(), x1.data_ptr()
+        m.triangles = tris.data_ptr() if len(mesh.triangles) else None
+        m.edges = edges.data_ptr() if len(mesh.edges) else None
+        h, nvf, nee = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64()
+        stream = torch.cuda.current_stream(dev)
+        rc = L.tccd_broad_create(ctypes.byref(m), float(inflation), ctypes.byref(h),
+                                 ctypes.byref(nvf), ctypes.byref(nee),
+                                 ctypes.c_void_p(stream.cuda_stream))
+        try:
+            _lib.check(rc, "tccd_broad_create")
+            total = nvf.value + nee.value
+            kind = torch.empty(total, dtype=torch.uint8, device=dev)
+            idx = torch.empty((total, 2), dtype=torch.int64, device=dev)
+            pts = torch.empty((total, 8, 3), dtype=torch.float64, device=dev)
+            _lib.check(L.tccd_broad_emit(h, ctypes.c_void_p(kind.data_ptr()),
+                                         ctypes.c_void_p(idx.data_ptr()),
+                                         ctypes.c_void_p(pts.data_ptr())), "tccd_broad_emit")
+        finally:
+            L.tccd_broad_destroy(h)
+    return CandidateSet(kind, idx, pts)
 
 
-def broad_phase(mesh: TriMeshPair, inflation: float = 0.0) -> list:
+def broad_phase(mesh: TriMeshPair, inflation: float = 0.0, device=None) -> list:
     """Reference-shaped result: a list of ContactCandidate."""
-    return broad_phase_batch(mesh, inflation).to_list()
+    return broad_phase_batch(mesh, inflation, device).to_list()
 
 
 def _solve(cs: CandidateSet, sel, cfg: SolverConfig, separation, device):
-    pts = torch.from_numpy(np.ascontiguousarray(cs.points[sel]))
-    kind = torch.from_numpy(np.ascontiguousarray(cs.kind[sel]))
-    sep = separation if np.isscalar(separation) else torch.from_numpy(
+    pts = torch.as_tensor(cs.points[sel])
+    kind = torch.as_tensor(cs.kind[sel])
+    sep = separation if np.isscalar(separation) else torch.as_tensor(
         np.ascontiguousarray(np.asarray(separation, dtype=np.float64)))
-    r = solve_batch(pts, kind, cfg, separation=sep, device=device)
-    return {k: v.numpy() for k, v in r.items()}
+    r = solve_batch(pts, kind, cfg, separation=sep, device=device if device is not None
+                    else (pts.device if pts.is_cuda else None))
+    return {k: _np(v) for k, v in r.items()}
 
 
 def _witness(r, i) -> DomainBox:
@@ -247,17 +232,34 @@ def _witness(r, i) -> DomainBox:
                      (float(w[4]), float(w[5])), int(r["level"][i]))
 
 
+def active_set_batch(mesh: TriMeshPair, delta: float = 1e-6, max_checks: int = 1_000_000,
+                     separation: float = 0.0, device=None):
+    """construct_active_set in batch form, device-resident: the broad phase
+    (inflation separation + delta) and one batched solve of every candidate
+    (scene.py:303-327).  Returns (hits, res): the colliding candidates as a
+    CandidateSet in candidate order, and their solver outputs (toi, witness,
+    level, ... as device tensors)."""
+    cs = broad_phase_batch(mesh, inflation=separation + delta, device=device)
+    cfg = SolverConfig(delta=delta, max_checks=max_checks, separation=separation)
+    if cs.m == 0:
+        return cs, {}
+    r = solve_batch(cs.points, cs.kind, cfg, device=cs.points.device)
+    hit = torch.nonzero(r["status"] == 1).squeeze(1)
+    hits = CandidateSet(cs.kind[hit], cs.indices[hit], cs.points[hit])
+    return hits, {k: v[hit] for k, v in r.items()}
+
+
 def construct_active_set(mesh: TriMeshPair, delta: float = 1e-6, max_checks: int = 1_000_000,
                          separation: float = 0.0, device=None) -> list:
     """Candidates the solver could not rule out, with toi and witness
-    (scene.py:303-327), from one batched solve."""
-    cs = broad_phase_batch(mesh, inflation=separation + delta)
-    if cs.m == 0:
+    (scene.py:303-327): active_set_batch as the reference's list of
+    (ContactCandidate, toi, DomainBox)."""
+    hits, r = active_set_batch(mesh, delta, max_checks, separation, device)
+    if hits.m == 0:
         return []
-    cfg = SolverConfig(delta=delta, max_checks=max_checks, separation=separation)
-    r = _solve(cs, slice(None), cfg, separation, device)
-    hits = np.flatnonzero(r["status"] == 1)
-    return [(cs.candidate(i), float(r["toi"][i]), _witness(r, i)) for i in hits]
+    hc = hits.host()
+    res = {k: _np(r[k]) for k in ("toi", "witness", "level")}
+    return [(hc.candidate(i), float(res["toi"][i]), _witness(res, i)) for i in range(hc.m)]
 
 
 # --- start-distance lower bounds: the reference's closed forms (scene.py:335-419),
@@ -385,17 +387,18 @@ def line_search_step(mesh: TriMeshPair, *, p: float, delta: float = 1e-6,
         raise ValueError("p must lie strictly between 0 and 1")
     if inflation is None:
         inflation = 2.0 * delta
-    cs = broad_phase_batch(mesh, inflation)
+    cs = broad_phase_batch(mesh, inflation, device=device)
+    hc = cs.host()
     m = cs.m
     d_lb = np.empty(m)
     eps_max = np.empty(m)
     for i in range(m):
-        d_lb[i] = distance_lb(int(cs.kind[i]), cs.points[i])
+        d_lb[i] = distance_lb(int(hc.kind[i]), hc.points[i])
         if d_lb[i] <= 0.0:
             raise InfeasibleStepError(
-                f"{QueryKind(int(cs.kind[i])).name} pair {tuple(int(x) for x in cs.indices[i])} "
+                f"{QueryKind(int(hc.kind[i])).name} pair {tuple(int(x) for x in hc.indices[i])} "
                 "touches at the step start; no positive step can be certified")
-        fe = compute_filters(QueryKind(int(cs.kind[i])), compute_gamma(cs.points[i]),
+        fe = compute_filters(QueryKind(int(hc.kind[i])), compute_gamma(hc.points[i]),
                              separation=min(p * d_lb[i], delta))
         eps_max[i] = max(fe.eps)
 
@@ -429,7 +432,7 @@ def line_search_step(mesh: TriMeshPair, *, p: float, delta: float = 1e-6,
                 toi = float(r["toi"][j]) if hit else None
                 # a free result carries codomain width 0 (solver.py:89-93)
                 achieved = max(achieved, float(r["codom"][j]) if hit else 0.0)
-                bounds.append(CandidateBound(cs.candidate(k), float(d_lb[k]), seps[k], toi,
+                bounds.append(CandidateBound(hc.candidate(k), float(d_lb[k]), seps[k], toi,
                                              _witness(r, j) if hit else None))
                 if hit and toi < alpha:
                     alpha = toi

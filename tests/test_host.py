@@ -190,22 +190,24 @@ def test_library_exports_every_header_symbol():
     assert b"unknown" in L.tccd_error_string(999)
 
 
-def test_struct_layout_matches_header(tmp_path):
-    """ctypes mirror of struct tccd_batch == the C compiler's layout."""
+@pytest.mark.parametrize("cname,pyname", [("tccd_batch", "TccdBatch"), ("tccd_mesh", "TccdMesh")])
+def test_struct_layout_matches_header(tmp_path, cname, pyname):
+    """ctypes mirrors of the C-ABI structs == the C compiler's layout."""
     from paper_2009_13349_b200 import _lib
-    fields = [f for f, _ in _lib.TccdBatch._fields_]
+    cls = getattr(_lib, pyname)
+    fields = [f for f, _ in cls._fields_]
     prog = ["#include <stdio.h>", "#include <stddef.h>", '#include "tccd.h"', "int main(void){",
-            'printf("%zu\\n", sizeof(tccd_batch));']
-    prog += [f'printf("%zu\\n", offsetof(tccd_batch, {f}));' for f in fields]
+            f'printf("%zu\\n", sizeof({cname}));']
+    prog += [f'printf("%zu\\n", offsetof({cname}, {f}));' for f in fields]
     prog += ["return 0;}"]
     c = tmp_path / "layout.c"
     c.write_text("\n".join(prog))
     exe = tmp_path / "layout"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(c)])
     vals = [int(x) for x in subprocess.check_output([str(exe)]).split()]
-    assert vals[0] == ctypes.sizeof(_lib.TccdBatch)
+    assert vals[0] == ctypes.sizeof(cls)
     for f, off in zip(fields, vals[1:]):
-        assert getattr(_lib.TccdBatch, f).offset == off, f
+        assert getattr(cls, f).offset == off, f
 
 
 def test_workspace_bytes_is_monotone_and_rejects_bad_sizes():

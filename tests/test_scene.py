@@ -15,11 +15,12 @@ import numpy as np
 import pytest
 
 from conftest import GOLDEN_DIR
-from paper_2009_13349_b200 import scene
+from paper_2009_13349_b200 import SolverConfig, scene
 from paper_2009_13349_b200.scene import (InfeasibleStepError, TriMeshPair, broad_phase,
                                          broad_phase_batch, construct_active_set,
                                          edges_from_triangles, line_search_step, load_obj,
                                          primitive_distance_lb)
+from scene_host import broad_phase_host
 
 with open(os.path.join(GOLDEN_DIR, "scene.json")) as _fh:
     GOLD = json.load(_fh)
@@ -38,32 +39,45 @@ def _bits(x):
 
 @pytest.fixture
 def oracle_device(monkeypatch):
-    """Route the scene module's batched solve through the CPU oracle."""
+    """Route the scene module's broad phase and batched solves through the
+    host checkers (tests/scene_host.py, the CPU oracle)."""
     import oracle
 
     def fake(cs, sel, cfg, separation, device):
         sep = separation if np.isscalar(separation) else np.asarray(separation, np.float64)
-        return oracle.solve_batch(cs.points[sel], cs.kind[sel], delta=cfg.delta,
-                                  max_checks=cfg.max_checks, separation=sep, t_max=cfg.t_max)
+        return oracle.solve_batch(np.asarray(cs.points[sel]), np.asarray(cs.kind[sel]),
+                                  delta=cfg.delta, max_checks=cfg.max_checks, separation=sep,
+                                  t_max=cfg.t_max)
+
+    def fake_active(mesh, delta=1e-6, max_checks=1_000_000, separation=0.0, device=None):
+        cs = broad_phase_host(mesh, separation + delta)
+        cfg = SolverConfig(delta=delta, max_checks=max_checks, separation=separation)
+        r = fake(cs, slice(None), cfg, separation, device)
+        hit = np.flatnonzero(r["status"] == 1)
+        return (scene.CandidateSet(cs.kind[hit], cs.indices[hit], cs.points[hit]),
+                {k: v[hit] for k, v in r.items()})
 
     monkeypatch.setattr(scene, "_solve", fake)
+    monkeypatch.setattr(scene, "broad_phase_batch", broad_phase_host)
+    monkeypatch.setattr(scene, "active_set_batch", fake_active)
+
+
+def _cand_list(cs):
+    h = cs.host()
+    return [[int(k), int(i), int(j)] for k, (i, j) in zip(h.kind, h.indices)]
 
 
 # ---------------------------------------------------------------- broad phase
 
 @pytest.mark.parametrize("tag", TAGS)
-def test_broad_phase_matches_reference(tag):
+def test_host_broad_phase_matches_reference(tag):
     mesh = _mesh(tag)
     for infl, want in GOLD[tag]["broad"].items():
-        cs = broad_phase_batch(mesh, float(infl))
-        got = [[int(k), int(i), int(j)] for k, (i, j) in zip(cs.kind, cs.indices)]
-        assert got == want, (tag, infl)
+        assert _cand_list(broad_phase_host(mesh, float(infl))) == want, (tag, infl)
 
 
-@pytest.mark.parametrize("tag", TAGS)
-def test_candidate_points_follow_solver_order(tag):
-    mesh = _mesh(tag)
-    for c in broad_phase(mesh, 0.3):
+def _check_points(mesh, cands):
+    for c in cands:
         if c.kind == 0:
             v, f = c.indices
             vid = [v, *mesh.triangles[f]]
@@ -75,12 +89,18 @@ def test_candidate_points_follow_solver_order(tag):
 
 
 @pytest.mark.parametrize("tag", TAGS)
+def test_candidate_points_follow_solver_order(tag):
+    mesh = _mesh(tag)
+    _check_points(mesh, broad_phase_host(mesh, 0.3).to_list())
+
+
+@pytest.mark.parametrize("tag", TAGS)
 def test_distance_lb_bitwise(tag):
-    got = [primitive_distance_lb(c) for c in broad_phase(_mesh(tag), 0.3)]
+    got = [primitive_distance_lb(c) for c in broad_phase_host(_mesh(tag), 0.3).to_list()]
     assert np.array_equal(_bits(got), _bits(GOLD[tag]["dlb"]))
 
 
-def test_broad_phase_random_against_brute_force():
+def test_host_broad_phase_random_against_brute_force():
     rng = np.random.default_rng(5)
     for trial in range(5):
         nv = 60
@@ -102,9 +122,7 @@ def test_broad_phase_random_against_brute_force():
         E = mesh.edges
         want += [[1, i, j] for i in range(len(E)) for j in range(i + 1, len(E))
                  if not set(E[i]) & set(E[j]) and ov(elo[i], ehi[i], elo[j], ehi[j])]
-        cs = broad_phase_batch(mesh, infl)
-        got = [[int(k), int(i), int(j)] for k, (i, j) in zip(cs.kind, cs.indices)]
-        assert got == want
+        assert _cand_list(broad_phase_host(mesh, infl)) == want
 
 
 def test_mesh_validation_and_edges(tmp_path):
@@ -121,7 +139,7 @@ def test_mesh_validation_and_edges(tmp_path):
     m = TriMeshPair(np.zeros((3, 3)), np.ones((3, 3)), [[0, 1, 2]], edges=np.zeros((0, 2)))
     assert m.edges.shape == (0, 2)
     assert np.array_equal(m.at(0.25), np.full((3, 3), 0.25))
-    assert broad_phase(TriMeshPair(np.zeros((0, 3)), np.zeros((0, 3)), [])) == []
+    assert broad_phase_host(TriMeshPair(np.zeros((0, 3)), np.zeros((0, 3)), [])).m == 0
     obj = tmp_path / "q.obj"
     obj.write_text("# quad\nv 0 0 0\nv 1 0 0\nv 1 1 0\nv 0 1 0\nvn 0 0 1\nf 1/1/1 2/2/1 3 -1\n")
     v, f = load_obj(obj)
@@ -131,7 +149,7 @@ def test_mesh_validation_and_edges(tmp_path):
         load_obj(obj)
 
 
-def test_touching_start_is_infeasible():
+def test_touching_start_is_infeasible(oracle_device):
     x = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0.25, 0.25, 0.0]])
     mesh = TriMeshPair(x, x + [0, 0, 0.1], [[0, 1, 2]])
     with pytest.raises(InfeasibleStepError):
@@ -199,6 +217,54 @@ def test_line_search_energy_loop(oracle_device):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("tag", TAGS)
+def test_gpu_broad_phase_matches_reference(tag):
+    mesh = _mesh(tag)
+    for infl, want in GOLD[tag]["broad"].items():
+        cs = broad_phase_batch(mesh, float(infl))
+        assert cs.points.is_cuda
+        assert _cand_list(cs) == want, (tag, infl)
+    _check_points(mesh, broad_phase(mesh, 0.3))
+
+
+def _random_meshes():
+    rng = np.random.default_rng(17)
+    for trial in range(4):  # soups of varying density
+        nt = [50, 400, 1500, 3000][trial]
+        c = rng.uniform(-1, 1, (nt, 1, 3))
+        v0 = (c + rng.normal(0, 0.04 * (4 - trial), (nt, 3, 3))).reshape(-1, 3)
+        yield f"soup{nt}", TriMeshPair(v0, v0 + rng.normal(0, 0.05, v0.shape),
+                                       np.arange(3 * nt).reshape(nt, 3))
+    g = 60  # a shared-vertex grid sheet folding onto itself
+    xs, ys = np.meshgrid(np.linspace(0, 1, g), np.linspace(0, 1, g))
+    x0 = np.stack([xs.ravel(), ys.ravel(), np.zeros(g * g)], 1)
+    x1 = x0 + np.stack([np.zeros(g * g), np.zeros(g * g), 0.3 * np.sin(6 * xs.ravel())], 1)
+    tris = []
+    for i in range(g - 1):
+        for j in range(g - 1):
+            a, b, c_, d = i * g + j, i * g + j + 1, (i + 1) * g + j, (i + 1) * g + j + 1
+            tris += [[a, b, c_], [b, d, c_]]
+    yield "sheet", TriMeshPair(x0, x1, tris)
+    yield "flat", TriMeshPair(x0, x0, tris)  # zero extent on z
+    z = np.zeros((5, 3))
+    yield "coincident", TriMeshPair(z, z, [[0, 1, 2], [2, 3, 4]])  # all boxes one point
+    yield "edges_only", TriMeshPair(x0[:40], x1[:40], np.zeros((0, 3)),
+                                    edges=np.array([[i, i + 1] for i in range(39)]))
+    yield "empty", TriMeshPair(np.zeros((0, 3)), np.zeros((0, 3)), [])
+
+
+@pytest.mark.gpu
+def test_gpu_broad_phase_matches_host_restatement():
+    for name, mesh in _random_meshes():
+        for infl in (0.0, 1e-3, 0.05):
+            want = broad_phase_host(mesh, infl)
+            got = broad_phase_batch(mesh, infl)
+            assert _cand_list(got) == _cand_list(want), (name, infl)
+            assert np.array_equal(got.points.cpu().numpy(), np.asarray(want.points)), name
+
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", TAGS)
 def test_active_set_gpu(tag):
     mesh = _mesh(tag)
     for sep in GOLD[tag]["active"]:
@@ -226,7 +292,7 @@ def test_line_search_gpu_matches_sequential_oracle_large():
     mesh = TriMeshPair(v0, v1, np.arange(3 * m).reshape(m, 3))
     p, delta = 0.5, 1e-6
     r = line_search_step(mesh, p=p, inflation=0.05)
-    cs = broad_phase_batch(mesh, 0.05)
+    cs = broad_phase_batch(mesh, 0.05).host()
     alpha, lim = 1.0, None
     for i in range(cs.m):
         sep = min(r.p * r.bounds[i].distance_lb, delta)
