@@ -37,6 +37,14 @@ from .core import DomainBox, Query, QueryKind, SolverConfig
 from .inclusion import compute_filters, compute_gamma
 from .solver import solve_batch
 
+__all__ = [
+    "TriMeshPair", "ContactCandidate", "CandidateBound", "LineSearchResult",
+    "InfeasibleStepError", "edges_from_triangles", "load_obj", "broad_phase",
+    "construct_active_set", "primitive_distance_lb", "line_search_step",
+    # batch forms (device-resident)
+    "CandidateSet", "broad_phase_batch", "active_set_batch", "distance_lb",
+]
+
 _SQRT3 = math.sqrt(3.0)
 _DISTANCE_SLACK = 1e-9  # scene.py:42-45
 
