@@ -17,7 +17,7 @@ if ROOT not in sys.path:
 
 GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
 GOLDEN_SETS = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
-                     if not os.path.basename(p).startswith("ds_"))  # ds_*: dataset-format fixtures
+                     if not os.path.basename(p).startswith(("ds_", "irf_")))  # dataset / IRF fixtures
 FIELDS = ("status", "toi", "tol", "codom", "checks", "early", "witness", "level")
 
 

@@ -63,3 +63,16 @@ def oracle_eps(pts, kind, sep):
                                           out.ctypes.data_as(ctypes.c_void_p))
     assert rc == 1
     return tuple(out)
+
+
+# --- IRF baseline: the C restatement vs the reference's
+# own irf_solve outputs (tests/golden/make_irf_golden.py)
+
+IRF_SETS = ("irf_kat", "irf_hc", "irf_c0", "irf_c1")
+
+
+@pytest.mark.parametrize("name", IRF_SETS)
+def test_oracle_irf_matches_reference(name):
+    g = load_golden(name)
+    got = oracle.irf_batch(g["points"], g["kind"], g["delta"], g["max_checks"], g["t_max"])
+    assert_same_results(got, g, name)
