@@ -180,6 +180,21 @@ int tccd_broad_create(const tccd_mesh *mesh, double inflation, tccd_broad **out,
 int tccd_broad_emit(tccd_broad *h, uint8_t *kind, int64_t *pairs, double *points);
 void tccd_broad_destroy(tccd_broad *h);
 
+/*
+ * IRF baseline <- ccdkit.baselines.irf_solve
+ * (pkg/src/ccdkit/baselines.py:123-206): outward-rounded interval
+ * bisection, best-first by (t_lo, level, push order), bit-identical to the
+ * reference for every query.  Uses the tccd_batch fields points, kind,
+ * delta, max_checks (any value; <= 0 returns the root box as an early
+ * hit), max_checks_max, t_max (finite, >= 0), the outputs, workspace /
+ * workspace_bytes, heavy_blocks (= second-pass slots, 0 = one per SM) and
+ * device_sms; separation, eps, stats and events are ignored.  Per-query
+ * invalid delta / t_max / kind -> status TCCD_STATUS_ERR_PARAM (the
+ * reference's ValueError), non-finite coordinates -> ERR_NONFINITE.
+ */
+size_t tccd_irf_workspace_bytes(int64_t n, int64_t max_checks_max, int32_t big_slots);
+int tccd_irf_batch(const tccd_batch *batch, void *stream);
+
 const char *tccd_error_string(int code);
 int tccd_abi_version(void);
 

@@ -10,9 +10,10 @@ reference's solve-side Python surface on top.
 from .core import CCDResult, DomainBox, Query, QueryKind, SolverConfig
 from .inclusion import FilterEps, compute_filters, compute_gamma
 from .solver import OUTPUT_FIELDS, shard_bounds, solve, solve_batch, solve_kernel, warm_up
+from .baselines import irf_batch, irf_solve
 
 __all__ = [
     "CCDResult", "DomainBox", "FilterEps", "OUTPUT_FIELDS", "Query", "QueryKind",
     "SolverConfig", "compute_filters", "compute_gamma", "shard_bounds", "solve",
-    "solve_batch", "solve_kernel", "warm_up",
+    "solve_batch", "solve_kernel", "warm_up", "irf_batch", "irf_solve",
 ]

@@ -88,6 +88,8 @@ EXPORTS = (
     "tccd_broad_create",
     "tccd_broad_emit",
     "tccd_broad_destroy",
+    "tccd_irf_workspace_bytes",
+    "tccd_irf_batch",
 )
 
 _lib = None
@@ -127,6 +129,10 @@ def lib() -> ctypes.CDLL:
         L.tccd_broad_emit.argtypes = [_vp, _vp, _vp, _vp]
         L.tccd_broad_destroy.restype = None
         L.tccd_broad_destroy.argtypes = [_vp]
+        L.tccd_irf_workspace_bytes.restype = ctypes.c_size_t
+        L.tccd_irf_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32]
+        L.tccd_irf_batch.restype = ctypes.c_int
+        L.tccd_irf_batch.argtypes = [ctypes.POINTER(TccdBatch), _vp]
         v = L.tccd_abi_version()
         if v != ABI_VERSION:
             raise RuntimeError(f"libtccd ABI {v} != expected {ABI_VERSION}")
