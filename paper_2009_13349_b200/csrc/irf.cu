@@ -9,9 +9,8 @@
 // domain side < delta) or the first box popped once the budget is spent is
 // the answer.  The pop order decides toi, witness and checks, so each query
 // keeps a real binary heap: one thread per query (queries fetched
-// dynamically), its heap in a global arena laid out warp-interleaved (entry
-// k of the 32 lanes of a warp is one contiguous 2 KB run, so the hot top of
-// the heaps is read coalesced).  A heap can hold at most checks + 1 boxes;
+// dynamically), its heap an 8-ary heap in a global arena (see Heap).  A heap
+// can hold at most checks + 1 boxes;
 // queries whose heap outgrows the first pass's capacity are re-run from the
 // root by a second pass with max_checks + 2 entries per slot (exact: the
 // search is deterministic).
@@ -102,78 +101,89 @@ struct Ctr {
   unsigned long long overflow; // queries handed to pass 2
 };
 
-// a heap of one lane: entry k at base + (k * 32) * 8 doubles (warp-interleaved)
+// The heap of one thread: an 8-ary min-heap of 16-byte keys (t_lo, then
+// level << 48 | seq: the tuple order of :144/:202, level < 2^16 and seq <
+// 2^48) with the boxes in a parallel array.  The 8 children of a node are
+// one 128-byte line, so a pop costs ~log8(n) dependent loads.
+struct Key {
+  double tl;
+  unsigned long long ls;  // level << 48 | seq
+};
+
+__device__ __forceinline__ bool key_less(const Key& a, const Key& b) {
+  return a.tl < b.tl || (a.tl == b.tl && a.ls < b.ls);  // t_lo is never NaN
+}
+
 struct Heap {
-  double* base;  // this lane's entry 0
+  Key* key;     // [cap]
+  double2* box; // [cap][3]: (tl, th), (ul, uh), (vl, vh)
   long long cap, n;
-  __device__ __forceinline__ double* at(long long k) const { return base + k * 256; }
-  __device__ __forceinline__ bool less(long long i, double tl, long long lv, long long sq) const {
-    const double* e = at(i);
-    const double ti = e[0];
-    if (ti != tl) return ti < tl;
-    const long long li = __double_as_longlong(e[6]);
-    if (li != lv) return li < lv;
-    return __double_as_longlong(e[7]) < sq;
+  __device__ __forceinline__ void load_box(long long i, double b[6]) const {
+    const double2 x = box[3 * i], y = box[3 * i + 1], z = box[3 * i + 2];
+    b[0] = x.x; b[1] = x.y; b[2] = y.x; b[3] = y.y; b[4] = z.x; b[5] = z.y;
   }
-  __device__ __forceinline__ void put(long long i, const double b[6], long long lv, long long sq) {
-    double* e = at(i);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) e[k] = b[k];
-    e[6] = __longlong_as_double(lv);
-    e[7] = __longlong_as_double(sq);
+  __device__ __forceinline__ void store_box(long long i, const double b[6]) {
+    box[3 * i] = make_double2(b[0], b[1]);
+    box[3 * i + 1] = make_double2(b[2], b[3]);
+    box[3 * i + 2] = make_double2(b[4], b[5]);
   }
   __device__ __forceinline__ void move(long long dst, long long src) {
-    double* d = at(dst);
-    const double* s = at(src);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) d[k] = s[k];
+    key[dst] = key[src];
+    box[3 * dst] = box[3 * src];
+    box[3 * dst + 1] = box[3 * src + 1];
+    box[3 * dst + 2] = box[3 * src + 2];
   }
-  __device__ void push(const double b[6], long long lv, long long sq) {
+  __device__ void push(const double b[6], unsigned long long ls) {
+    const Key k{b[0], ls};
     long long i = n++;
     while (i > 0) {
-      const long long p = (i - 1) >> 1;
-      if (!less_key(b[0], lv, sq, p)) break;
+      const long long p = (i - 1) >> 3;
+      const Key kp = key[p];
+      if (!key_less(k, kp)) break;
       move(i, p);
       i = p;
     }
-    put(i, b, lv, sq);
+    key[i] = k;
+    store_box(i, b);
   }
-  // (tl, lv, sq) < entry p ?
-  __device__ __forceinline__ bool less_key(double tl, long long lv, long long sq, long long p) const {
-    const double* e = at(p);
-    const double tp = e[0];
-    if (tl != tp) return tl < tp;
-    const long long lp = __double_as_longlong(e[6]);
-    if (lv != lp) return lv < lp;
-    return sq < __double_as_longlong(e[7]);
+  __device__ __forceinline__ void top(double b[6], unsigned long long& ls) const {
+    ls = key[0].ls;
+    load_box(0, b);
   }
-  __device__ void pop(double b[6], long long& lv) {
-    const double* top = at(0);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) b[k] = top[k];
-    lv = __double_as_longlong(top[6]);
-    --n;
-    if (n == 0) return;
-    double last[8];
-    const double* le = at(n);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) last[k] = le[k];
-    const long long llv = __double_as_longlong(last[6]), lsq = __double_as_longlong(last[7]);
+  // put (k, b) at the root's place and sift it down
+  __device__ void sift_down_from_root(const Key& k, const double b[6]) {
     long long i = 0;
     for (;;) {
-      long long c = 2 * i + 1;
-      if (c >= n) break;
-      if (c + 1 < n) {
-        const double* e1 = at(c + 1);
-        if (less(c, e1[0], __double_as_longlong(e1[6]), __double_as_longlong(e1[7])) == false) ++c;
+      const long long c0 = 8 * i + 1;
+      if (c0 >= n) break;
+      const long long cend = c0 + 8 < n ? c0 + 8 : n;
+      long long c = c0;
+      Key kc = key[c0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) {
+        if (c0 + j < cend) {
+          const Key kj = key[c0 + j];
+          if (key_less(kj, kc)) { kc = kj; c = c0 + j; }
+        }
       }
-      if (!less(c, last[0], llv, lsq)) break;
+      if (!key_less(kc, k)) break;
       move(i, c);
       i = c;
     }
-    double* d = at(i);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) d[k] = last[k];
+    key[i] = k;
+    store_box(i, b);
+  }
+  __device__ void pop_discard() {  // remove the root
+    if (--n == 0) return;
+    const Key last = key[n];
+    double lb[6];
+    load_box(n, lb);
+    sift_down_from_root(last, lb);
+  }
+  // replace the root by (b, ls): a popped box's first child usually sinks
+  // only a level or two, where pop + push would sift it up the whole path
+  __device__ void replace_top(const double b[6], unsigned long long ls) {
+    sift_down_from_root(Key{b[0], ls}, b);
   }
 };
 
@@ -200,12 +210,13 @@ __device__ bool irf_query(const Args& a, long long q, Heap& H) {
   if (st == 0) {
     H.n = 0;
     const double root[6] = {0.0, t_max, 0.0, 1.0, 0.0, 1.0};
-    H.push(root, 0, 0);
-    long long seq = 0;
+    H.push(root, 0ull);
+    unsigned long long seq = 0;
     while (H.n > 0) {
       double b[6];
-      long long lv;
-      H.pop(b, lv);
+      unsigned long long ls;
+      H.top(b, ls);  // popped below, or replaced by its first child
+      const long long lv = (long long)(ls >> 48);
       const Iv t{b[0], b[1]}, u{b[2], b[3]}, v{b[4], b[5]};
       const bool budget = checks >= mc;  // :147-165
       bool all = true;
@@ -224,7 +235,10 @@ __device__ bool irf_query(const Args& a, long long q, Heap& H) {
         break;
       }
       ++checks;
-      if (!all) continue;
+      if (!all) {
+        H.pop_discard();
+        continue;
+      }
       const double wt = b[1] - b[0], wu = b[3] - b[2], wv = b[5] - b[4];
       double mw = wt;
       int dim = 0;  // np.argmax: first maximum
@@ -235,16 +249,30 @@ __device__ bool irf_query(const Args& a, long long q, Heap& H) {
         for (int k = 0; k < 6; ++k) w[k] = b[k];
         break;
       }
-      const double m = 0.5 * (b[2 * dim] + b[2 * dim + 1]);
+      // (selects, not b[2 * dim]: a dynamic index would put the box in local memory)
+      const double lo_d = dim == 0 ? b[0] : (dim == 1 ? b[2] : b[4]);
+      const double hi_d = dim == 0 ? b[1] : (dim == 1 ? b[3] : b[5]);
+      const double m = 0.5 * (lo_d + hi_d);
       double k0[6], k1[6];
-      for (int k = 0; k < 6; ++k) { k0[k] = b[k]; k1[k] = b[k]; }
-      k0[2 * dim + 1] = m;
-      k1[2 * dim] = m;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        k0[k] = (k == 2 * dim + 1) ? m : b[k];
+        k1[k] = (k == 2 * dim) ? m : b[k];
+      }
       const bool keep0 = !(kind == 0 && k0[2] + k0[4] > 1.0);  // :197-199
       const bool keep1 = !(kind == 0 && k1[2] + k1[4] > 1.0);
-      if (H.n + (keep0 ? 1 : 0) + (keep1 ? 1 : 0) > H.cap) return false;
-      if (keep0) H.push(k0, lv + 1, ++seq);
-      if (keep1) H.push(k1, lv + 1, ++seq);
+      if (H.n - 1 + (keep0 ? 1 : 0) + (keep1 ? 1 : 0) > H.cap) return false;
+      // (level <= 3 * 1075: each split halves one side of a binary64 box)
+      const unsigned long long lv1 = (unsigned long long)(lv + 1) << 48;
+      if (keep0 && keep1) {
+        const unsigned long long s0 = lv1 | ++seq, s1 = lv1 | ++seq;
+        H.replace_top(k0, s0);
+        H.push(k1, s1);
+      } else if (keep0 || keep1) {
+        H.replace_top(keep0 ? k0 : k1, lv1 | ++seq);
+      } else {
+        H.pop_discard();
+      }
     }
   }
   a.status[q] = st;
@@ -259,14 +287,16 @@ __device__ bool irf_query(const Args& a, long long q, Heap& H) {
   return true;
 }
 
-// pass 0: every query (index list = identity); pass 1: the overflow list
-__global__ void __launch_bounds__(128) irf_kernel(Args a, Ctr* ctr, double* arena, long long cap,
-                                                  const long long* list, long long* overflow,
-                                                  int pass) {
+// pass 0: every query (index list = identity); pass 1: the overflow list.
+// Per thread: cap keys (16 B) then cap boxes (48 B), contiguous.
+__global__ void __launch_bounds__(128) irf_kernel(Args a, Ctr* ctr, unsigned char* arena,
+                                                  long long cap, const long long* list,
+                                                  long long* overflow, int pass) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
   Heap H;
-  H.base = arena + ((tid >> 5) * cap * 32 + lane) * 8;
+  unsigned char* mine = arena + tid * cap * 64;
+  H.key = (Key*)mine;
+  H.box = (double2*)(mine + cap * 16);
   H.cap = cap;
   H.n = 0;
   const unsigned long long total = pass == 0 ? (unsigned long long)a.n : ctr->overflow;
@@ -287,7 +317,7 @@ using namespace tccd_irf;
 
 namespace {
 
-constexpr long long kCap1 = 256;   // heap entries per thread in pass 1
+constexpr long long kCap1 = 2048;  // heap entries per thread in pass 1
 constexpr int kThreads = 128;
 
 size_t a256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -297,11 +327,29 @@ struct IrfLayout {
   long long threads1, slots2, cap2;
 };
 
+int resident_blocks() {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, irf_kernel, kThreads, 0) != cudaSuccess ||
+      nb < 1)
+    nb = 2;
+  return nb;
+}
+
+// slots2 <= 0: as many second-pass threads as a quarter of the device
+// memory holds (one per SM at least, 4096 at most)
 IrfLayout irf_layout(long long n, long long mcmax, int slots2, int sms) {
   IrfLayout L;
-  L.threads1 = (long long)sms * 8 * kThreads;  // 8 blocks of 128 per SM
-  L.slots2 = ((long long)(slots2 > 0 ? slots2 : sms) + 31) / 32 * 32;
+  L.threads1 = (long long)sms * resident_blocks() * kThreads;
   L.cap2 = (mcmax > 0 ? mcmax : 0) + 2;
+  long long s2 = slots2;
+  if (s2 <= 0) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) tot = (size_t)16 << 30;
+    s2 = (long long)(tot / 4 / ((size_t)L.cap2 * 64));
+    if (s2 > 4096) s2 = 4096;
+    if (s2 < sms) s2 = sms;
+  }
+  L.slots2 = (s2 + 31) / 32 * 32;
   size_t o = 0;
   L.ctr = o; o += a256(sizeof(Ctr));
   L.overflow = o; o += a256((size_t)(n > 0 ? n : 1) * 8);
@@ -367,11 +415,11 @@ int tccd_irf_batch(const tccd_batch* b, void* stream) {
   long long* ovf = (long long*)(ws + L.overflow);
   if (cudaMemsetAsync(ctr, 0, sizeof(Ctr), st) != cudaSuccess) return TCCD_E_CUDA;
   irf_kernel<<<(unsigned)(L.threads1 / kThreads), kThreads, 0, st>>>(
-      a, ctr, (double*)(ws + L.arena1), kCap1, nullptr, ovf, 0);
+      a, ctr, ws + L.arena1, kCap1, nullptr, ovf, 0);
   if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
   // pass 2 (a no-op when nothing overflowed): max_checks + 2 entries per slot
-  irf_kernel<<<(unsigned)(L.slots2 / 32), 32, 0, st>>>(a, ctr, (double*)(ws + L.arena2), L.cap2,
-                                                       ovf, ovf, 1);
+  irf_kernel<<<(unsigned)(L.slots2 / 32), 32, 0, st>>>(a, ctr, ws + L.arena2, L.cap2, ovf, ovf,
+                                                       1);
   if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
   return TCCD_OK;
 }

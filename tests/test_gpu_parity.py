@@ -277,13 +277,22 @@ def test_benchmark_harness_matches_reference(cuda, name, tag):
     from paper_2009_13349_b200.dataset import parse_queries
     kind = QueryKind.VERTEX_FACE if tag == "vf" else QueryKind.EDGE_EDGE
     g = np.load(os.path.join(GOLDEN_DIR, f"ds_{name}_{tag}.npz"))
-    rep = run_benchmark(parse_queries(os.path.join(GOLDEN_DIR, f"ds_{name}_{tag}.csv"), kind),
-                        device=cuda)
+    data = parse_queries(os.path.join(GOLDEN_DIR, f"ds_{name}_{tag}.csv"), kind)
+    rep = run_benchmark(data, ("irf", "OURS", "ours"), device=cuda)
+    assert [m.name for m in rep.methods] == ["ours", "irf"]
     m = rep.method("ours")
     assert np.array_equal(np.array(m.verdicts), g["verdicts"])
     assert (m.fp_count, m.fn_count, m.correct_count, m.early_count) == \
         (int(g["fp"]), int(g["fn"]), int(g["correct"]), int(g["early"]))
     assert sum(m.histogram) == rep.size and rep.queries_per_second > 0
+    # the IRF method's verdicts: the oracle's restatement of irf_solve with
+    # the config's delta / max_checks / t_max (bench.py:169-175)
+    ref = oracle.irf_batch(data.points, data.kind, 1e-6, 1_000_000, 1.0)
+    mi = rep.method("irf")
+    assert np.array_equal(np.array(mi.verdicts), ref["status"] == 1)
+    assert mi.fn_count == 0 and mi.early_count == int(ref["early"].sum())
+    with pytest.raises(ValueError):
+        run_benchmark(data, ("univariate",), device=cuda)
 
 
 def test_cli_run_and_fn_guard(cuda, tmp_path):
