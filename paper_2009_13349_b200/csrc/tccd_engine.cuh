@@ -1009,7 +1009,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       unsigned int* const outr = pick(ar.ref, nxt);
       uint8_t* const sln = pick(slot_of, nxt);
       uint8_t* const fln = pick(flags, nxt);
+      // (only deferred levels copy non-refining boxes: without deferrals this
+      // round, the chunk mask settles those boxes without touching them)
+      const bool any_deferred = S.deferred_last != 0;
       for (int i = tid; i < n; i += NT) {
+        if (!any_deferred && !((ch.m[kMR][i >> 5] >> (i & 31)) & 1u)) continue;
         const int s = sl[i];
         const int cs = S.cont[s];
         if (cs == 0) continue;
