@@ -327,3 +327,26 @@ def test_non_blocking_host_pipeline(cuda):
         g["ready"].synchronize()
         for key in ("status", "toi", "checks", "witness", "level"):
             assert torch.equal(g[key], r[key]), key
+
+
+def test_multi_chunk_batch(cuda):
+    """A batch above the library's 2^22-query chunk (BASELINE config 3 is
+    5e7 queries): results do not depend on chunking -- the queries around
+    the chunk boundary, solved alone and inside the big batch, agree with
+    each other and with the oracle."""
+    from paper_2009_13349_b200 import solve_batch
+    from paper_2009_13349_b200 import workloads as W
+    n = (1 << 22) + 50_000
+    w = W.generate(3, 0, n)
+    pts = torch.from_numpy(w.points).to(cuda)
+    kind = torch.from_numpy(w.kind).to(cuda)
+    big = solve_batch(pts, kind, device=cuda)
+    lo, hi = (1 << 22) - 3_000, (1 << 22) + 3_000
+    alone = solve_batch(pts[lo:hi], kind[lo:hi], device=cuda)
+    for k in ("status", "toi", "checks", "witness", "level"):
+        assert torch.equal(big[k][lo:hi], alone[k]), k
+    ref = oracle.solve_batch(w.points[lo:hi], w.kind[lo:hi], w.delta, w.max_checks)
+    assert_same_results({k: v[lo:hi].cpu().numpy() for k, v in big.items()}, ref, "chunk edge")
+    tail = slice(n - 2_000, n)
+    ref = oracle.solve_batch(w.points[tail], w.kind[tail], w.delta, w.max_checks)
+    assert_same_results({k: v[tail].cpu().numpy() for k, v in big.items()}, ref, "last chunk")
