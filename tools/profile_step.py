@@ -30,12 +30,16 @@ if args.config == 2:
     kw = dict(delta=torch.from_numpy(w.delta).to(dev), max_checks=torch.from_numpy(w.max_checks).to(dev))
 for r in range(args.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     e0.record()
     out = solve_batch(pts, kind, outputs=("status", "toi", "checks"), device=dev,
-                      separation=w.separation, heavy_only=args.heavy_only, stats=True, **kw)
+                      separation=w.separation, heavy_only=args.heavy_only, stats=True,
+                      events=ev, **kw)
     e1.record()
     torch.cuda.synchronize()
     st = out["stats"].tolist()
-    print(f"rep {r}: {e0.elapsed_time(e1):.2f} ms  checks {int(out['checks'].sum())} "
+    stages = [e0.elapsed_time(ev[0])] + [ev[j].elapsed_time(ev[j + 1]) for j in range(3)]
+    print(f"rep {r}: {e0.elapsed_time(e1):.2f} ms  stages " + "/".join(f"{x:.2f}" for x in stages) +
+          f"  checks {int(out['checks'].sum())} "
           f"giant {st[0]} medium {st[3]} rounds {st[1]} deferrals {st[2]} "
           f"boxes L/M/G {st[4]}/{st[5]}/{st[6]}", flush=True)
