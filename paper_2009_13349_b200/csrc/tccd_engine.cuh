@@ -533,7 +533,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     }
     gsync<G>();
     TCCD_PHASE(0);
-    const int k_adm = S.admit_k;
+    const int k_adm = S.admit_k;  // (group-uniform: branch and barriers below are safe)
+    if (k_adm > 0) {
     // step 1a: free slot of each admitted entry
     for (int s = tid; s < Q; s += NT) {
       if (S.qidx[s] < 0 && k_adm > 0) {
@@ -600,6 +601,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         pos += S.adm_n[r];
       }
       S.n_next = pos;  // new fill (reused as scratch until P5)
+      S.n_cur = pos;
     }
     gsync<G>();
     // step 3: reference lists of the admitted levels
@@ -621,6 +623,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         }
       }
     }
+    }  // k_adm > 0
     for (int s = tid; s < Q; s += NT) {
       S.hoff[s] = -1;
       S.j[s] = kIntMax;
@@ -630,8 +633,6 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     }
     gsync<G>();
     TCCD_PHASE(1);
-    if (tid == 0) { S.n_cur = k_adm > 0 ? S.n_next : S.n_cur; S.any_general = 0; }
-    gsync<G>();
     TCCD_PHASE(2);
     const int n = S.n_cur;
     if (n == 0) break;
