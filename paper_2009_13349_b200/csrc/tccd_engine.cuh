@@ -407,6 +407,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   // another (G = 32: warp-synchronous, no block barriers).
   constexpr int G = Cfg::G, Q = Cfg::Q;
   constexpr int NT = G;  // stride of the per-group loops
+  // one query per group (giant tier): every box belongs to slot 0, so the
+  // per-box slot bytes are never read
+  constexpr bool ONEQ = Q == 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int group = threadIdx.x / G;
   unsigned char* gsmem = smem_raw + (size_t)group * engine_smem_bytes<Cfg>();
@@ -637,7 +640,6 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     const int n = S.n_cur;
     if (n == 0) break;
     ++rounds;
-    boxes += (unsigned long long)n;
     Box* const bx = pick(ar.box, cur);
     const Box* const bprev = pick(ar.box, prv);
     double* const wbc = pick(ar.wb, cur);
@@ -650,25 +652,30 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     // box i + NT are in flight while box i is classified
     // (handed-over boxes are read from the tier's handover pool)
     const Box* const pool = io.in_pbox;
-    unsigned int r_cur = tid < n ? rf[tid] : kRefRoot;
+    // one query: boxes past its budget cut are never classified, and the query
+    // ends this round (P3), so the round stops at the cut
+    const int n1 = ONEQ ? (int)min((long long)n, S.seg_off[0] + max(S.qp[0].max_checks - S.C[0], 0ll))
+                        : n;
+    boxes += (unsigned long long)n1;
+    unsigned int r_cur = tid < n1 ? rf[tid] : kRefRoot;
     Box p_cur;
     if (!(r_cur & kRefRoot)) p_cur = bprev[r_cur & kRefSrcMask];
     else if ((r_cur & kRefExt) == kRefExt) p_cur = pool[r_cur & kRefSrcMask];
-    unsigned int r_nxt = tid + NT < n ? rf[tid + NT] : kRefRoot;
+    unsigned int r_nxt = tid + NT < n1 ? rf[tid + NT] : kRefRoot;
     // (warp-uniform trip count: every lane reaches the chunk ballots)
-    for (int i = tid; i - lane < n; i += NT) {
+    for (int i = tid; i - lane < n1; i += NT) {
       Box p_nxt;
       if (!(r_nxt & kRefRoot)) p_nxt = bprev[r_nxt & kRefSrcMask];
       else if ((r_nxt & kRefExt) == kRefExt) p_nxt = pool[r_nxt & kRefSrcMask];
-      const unsigned int r_nn = i + 2 * NT < n ? rf[i + 2 * NT] : kRefRoot;
+      const unsigned int r_nn = i + 2 * NT < n1 ? rf[i + 2 * NT] : kRefRoot;
       const unsigned int r = r_cur;
       const Box p = p_cur;
       r_cur = r_nxt;
       p_cur = p_nxt;
       r_nxt = r_nn;
       uint8_t f = 0;
-      if (i < n) {
-      const int s = sl[i];
+      if (i < n1) {
+      const int s = ONEQ ? 0 : sl[i];
       const QueryParams& qp = S.qp[s];
       Box b;
       f = fl[i];  // head bit (+ class, for roots and deferred boxes)
@@ -804,6 +811,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     }
     gsync<G>();
     TCCD_PHASE(4);
+    const int nxt = prv;
+    // one query that ended this round: no next level to build
+    const bool build_next = !(ONEQ && S.cont[0] == 0);
+    if (!build_next && tid == 0) { S.n_next = 0; S.deferred_last = 0; }
+    if (build_next) {
     // ================= P4: chunk scan -> flat prefixes (A, B, refining boxes P)
     // Threads own contiguous ranges of 32-box chunks (one or two chunks each
     // in the shared-memory tiers).  Every query's boxes are counted (also
@@ -1005,7 +1017,6 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     //   rank(lower) = M + P,  rank(upper) = N + P   (segment-relative).
     // New run heads: the children of the first refining box of a run.
     // Lane per box; P, M, N and A from the chunk masks in O(1).
-    const int nxt = prv;
     {
       unsigned int* const outr = pick(ar.ref, nxt);
       uint8_t* const sln = pick(slot_of, nxt);
@@ -1014,42 +1025,52 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       // round, the chunk mask settles those boxes without touching them)
       const bool any_deferred = S.deferred_last != 0;
       for (int i = tid; i < n; i += NT) {
-        if (!any_deferred && !((ch.m[kMR][i >> 5] >> (i & 31)) & 1u)) continue;
-        const int s = sl[i];
+        const int c = i >> 5, l = i & 31;
+        const unsigned int lm = lowmask(l), bit = 1u << l;
+        // (one query: the chunk words are global; issue them together)
+        unsigned int R = ch.m[kMR][c], H, T, U;
+        int cP, cM, cN, cA;
+        if constexpr (ONEQ) {
+          H = ch.m[kMH][c]; T = ch.m[kMT][c]; U = ch.m[kMU][c];
+          cP = ch.c[kCP][c]; cM = ch.c[kCM][c]; cN = ch.c[kCN][c]; cA = ch.c[kCA][c];
+        }
+        if (!any_deferred && !(R & bit)) continue;
+        const int s = ONEQ ? 0 : sl[i];
         const int cs = S.cont[s];
         if (cs == 0) continue;
-        const uint8_t f = fl[i];
         if (cs == 2) {
           const int pos = S.next_off[s] + (i - S.seg_off[s]);
           outr[pos] = (unsigned)i | kRefSelf;
           sln[pos] = (uint8_t)s;
-          fln[pos] = f;
+          fln[pos] = fl[i];
           continue;
         }
-        if ((f & 3) == kDisjoint || (f & 4) || !S.uniform[s]) continue;
+        // refining boxes only; their split dimension and clipped upper child
+        // are in the chunk masks (T: t split, U: u / v split with an upper child)
+        if (!(R & bit) || !S.uniform[s]) continue;
         const bool hand = cs == 3 && S.hoff[s] >= 0;
         if (cs != 1 && !hand) continue;
-        const int c = i >> 5, l = i & 31;
-        const unsigned int lm = lowmask(l), bit = 1u << l;
-        const unsigned int R = ch.m[kMR][c], H = ch.m[kMH][c];
-        const int cP = ch.c[kCP][c];
+        if constexpr (!ONEQ) {
+          H = ch.m[kMH][c]; T = ch.m[kMT][c]; U = ch.m[kMU][c];
+          cP = ch.c[kCP][c]; cM = ch.c[kCM][c]; cN = ch.c[kCN][c]; cA = ch.c[kCA][c];
+        }
         const int Pr = cP + __popc(R & lm);
         const unsigned int hle = H & (lm | bit), hgt = H & ~(lm | bit);
-        const int M = hle ? cP + __popc(R & lowmask(31 - __clz(hle))) : ch.c[kCM][c];
-        int N = hgt ? cP + __popc(R & lowmask(__ffs(hgt) - 1)) : ch.c[kCN][c];
+        const int M = hle ? cP + __popc(R & lowmask(31 - __clz(hle))) : cM;
+        int N = hgt ? cP + __popc(R & lowmask(__ffs(hgt) - 1)) : cN;
         if (N > S.segP1[s]) N = S.segP1[s];  // the last run ends at the segment end
         const int S0 = S.segP0[s];
-        const int sdim = (f >> 3) & 3;
+        const bool tsplit = (T & bit) != 0;
         const uint8_t hd = Pr == M ? kHead : 0;
         int rl, ru = -1;
-        if (sdim == 0) {
+        if (tsplit) {
           rl = (M - S0) + (Pr - S0);
           ru = (N - S0) + (Pr - S0);
         } else {
-          rl = ch.c[kCA][c] + __popc(R & lm) + __popc(ch.m[kMU][c] & lm) - S.segA0[s];
-          if (f & 32) ru = rl + 1;
+          rl = cA + __popc(R & lm) + __popc(U & lm) - S.segA0[s];
+          if (U & bit) ru = rl + 1;
         }
-        const uint8_t hu = sdim == 0 ? hd : 0;
+        const uint8_t hu = tsplit ? hd : 0;
         if (!hand) {
           const int base = S.next_off[s];
           outr[base + rl] = (unsigned)i;
@@ -1183,6 +1204,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     }
     gsync<G>();
     }  // any_general
+    }  // build_next
     // ================= P7: commit
     for (int s = tid; s < Q; s += NT) {
       if (S.cont[s] == 1) {
