@@ -662,8 +662,16 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     if (!(r_cur & kRefRoot)) p_cur = bprev[r_cur & kRefSrcMask];
     else if ((r_cur & kRefExt) == kRefExt) p_cur = pool[r_cur & kRefSrcMask];
     unsigned int r_nxt = tid + NT < n1 ? rf[tid + NT] : kRefRoot;
+    // (global flags: prefetched one iteration ahead as well)
+    uint8_t f_cur = 0;
+    if constexpr (!Cfg::SMEM) f_cur = tid < n1 ? fl[tid] : 0;
     // (warp-uniform trip count: every lane reaches the chunk ballots)
     for (int i = tid; i - lane < n1; i += NT) {
+      uint8_t f_pre = 0;
+      if constexpr (!Cfg::SMEM) {
+        f_pre = f_cur;
+        f_cur = i + NT < n1 ? fl[i + NT] : 0;
+      }
       Box p_nxt;
       if (!(r_nxt & kRefRoot)) p_nxt = bprev[r_nxt & kRefSrcMask];
       else if ((r_nxt & kRefExt) == kRefExt) p_nxt = pool[r_nxt & kRefSrcMask];
@@ -678,7 +686,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       const int s = ONEQ ? 0 : sl[i];
       const QueryParams& qp = S.qp[s];
       Box b;
-      f = fl[i];  // head bit (+ class, for roots and deferred boxes)
+      f = Cfg::SMEM ? fl[i] : f_pre;  // head bit (+ class, for roots and deferred boxes)
       double wb = 0.0;
       if ((r & kRefExt) == kRefExt) {
         b = p;  // handed over (unclassified)
@@ -1024,6 +1032,57 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       // (only deferred levels copy non-refining boxes: without deferrals this
       // round, the chunk mask settles those boxes without touching them)
       const bool any_deferred = S.deferred_last != 0;
+      if (ONEQ && S.cont[0] == 1 && S.uniform[0]) {
+        // one continuing query: warp per chunk, the chunk words (global) of the
+        // warp's next chunk in flight while this one is placed; slot bytes
+        // are not written (only the general ordering path reads them)
+        constexpr int CS = NT / 32;
+        const int nch = (n + 31) >> 5;
+        const int base = S.next_off[0], S0 = S.segP0[0], S1 = S.segP1[0], A0 = S.segA0[0];
+        const unsigned int lm = lowmask(lane), bit = 1u << lane;
+        int c = tid >> 5;
+        unsigned int R = 0, H = 0, T = 0, U = 0;
+        int cP = 0, cM = 0, cN = 0, cA = 0;
+        if (c < nch) {
+          R = ch.m[kMR][c]; H = ch.m[kMH][c]; T = ch.m[kMT][c]; U = ch.m[kMU][c];
+          cP = ch.c[kCP][c]; cM = ch.c[kCM][c]; cN = ch.c[kCN][c]; cA = ch.c[kCA][c];
+        }
+        for (; c < nch; c += CS) {
+          unsigned int R2 = 0, H2 = 0, T2 = 0, U2 = 0;
+          int cP2 = 0, cM2 = 0, cN2 = 0, cA2 = 0;
+          if (c + CS < nch) {
+            const int d = c + CS;
+            R2 = ch.m[kMR][d]; H2 = ch.m[kMH][d]; T2 = ch.m[kMT][d]; U2 = ch.m[kMU][d];
+            cP2 = ch.c[kCP][d]; cM2 = ch.c[kCM][d]; cN2 = ch.c[kCN][d]; cA2 = ch.c[kCA][d];
+          }
+          if (R & bit) {
+            const int Pr = cP + __popc(R & lm);
+            const unsigned int hle = H & (lm | bit), hgt = H & ~(lm | bit);
+            const int M = hle ? cP + __popc(R & lowmask(31 - __clz(hle))) : cM;
+            int N = hgt ? cP + __popc(R & lowmask(__ffs(hgt) - 1)) : cN;
+            if (N > S1) N = S1;
+            const bool tsplit = (T & bit) != 0;
+            const uint8_t hd = Pr == M ? kHead : 0;
+            const int i = c * 32 + lane;
+            int rl, ru = -1;
+            if (tsplit) {
+              rl = (M - S0) + (Pr - S0);
+              ru = (N - S0) + (Pr - S0);
+            } else {
+              rl = cA + __popc(R & lm) + __popc(U & lm) - A0;
+              if (U & bit) ru = rl + 1;
+            }
+            outr[base + rl] = (unsigned)i;
+            fln[base + rl] = hd;
+            if (ru >= 0) {
+              outr[base + ru] = (unsigned)i | kRefCb;
+              fln[base + ru] = tsplit ? hd : 0;
+            }
+          }
+          R = R2; H = H2; T = T2; U = U2;
+          cP = cP2; cM = cM2; cN = cN2; cA = cA2;
+        }
+      } else
       for (int i = tid; i < n; i += NT) {
         const int c = i >> 5, l = i & 31;
         const unsigned int lm = lowmask(l), bit = 1u << l;
