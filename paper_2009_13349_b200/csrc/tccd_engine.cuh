@@ -1033,44 +1033,45 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       // round, the chunk mask settles those boxes without touching them)
       const bool any_deferred = S.deferred_last != 0;
       if (ONEQ && S.cont[0] == 1 && S.uniform[0]) {
-        // one continuing query: warp per chunk, the chunk words (global) of the
-        // warp's next chunk in flight while this one is placed; slot bytes
-        // are not written (only the general ordering path reads them)
+        // one continuing query: warp per chunk, the chunk words (global) of
+        // several chunks in flight together; slot bytes are not written (only
+        // the general ordering path reads them)
         constexpr int CS = NT / 32;
         const int nch = (n + 31) >> 5;
         const int base = S.next_off[0], S0 = S.segP0[0], S1 = S.segP1[0], A0 = S.segA0[0];
         const unsigned int lm = lowmask(lane), bit = 1u << lane;
-        int c = tid >> 5;
-        unsigned int R = 0, H = 0, T = 0, U = 0;
-        int cP = 0, cM = 0, cN = 0, cA = 0;
-        if (c < nch) {
-          R = ch.m[kMR][c]; H = ch.m[kMH][c]; T = ch.m[kMT][c]; U = ch.m[kMU][c];
-          cP = ch.c[kCP][c]; cM = ch.c[kCM][c]; cN = ch.c[kCN][c]; cA = ch.c[kCA][c];
-        }
-        for (; c < nch; c += CS) {
-          unsigned int R2 = 0, H2 = 0, T2 = 0, U2 = 0;
-          int cP2 = 0, cM2 = 0, cN2 = 0, cA2 = 0;
-          if (c + CS < nch) {
-            const int d = c + CS;
-            R2 = ch.m[kMR][d]; H2 = ch.m[kMH][d]; T2 = ch.m[kMT][d]; U2 = ch.m[kMU][d];
-            cP2 = ch.c[kCP][d]; cM2 = ch.c[kCM][d]; cN2 = ch.c[kCN][d]; cA2 = ch.c[kCA][d];
+        // four chunks per pass: their 32 words are loaded together
+        constexpr int UN = 4;
+        for (int c0 = tid >> 5; c0 < nch; c0 += UN * CS) {
+          unsigned int R[UN], H[UN], T[UN], U[UN];
+          int cP[UN], cM[UN], cN[UN], cA[UN];
+#pragma unroll
+          for (int u = 0; u < UN; ++u) {
+            const int c = c0 + u * CS;
+            R[u] = 0; H[u] = 0; T[u] = 0; U[u] = 0; cP[u] = 0; cM[u] = 0; cN[u] = 0; cA[u] = 0;
+            if (c < nch) {
+              R[u] = ch.m[kMR][c]; H[u] = ch.m[kMH][c]; T[u] = ch.m[kMT][c]; U[u] = ch.m[kMU][c];
+              cP[u] = ch.c[kCP][c]; cM[u] = ch.c[kCM][c]; cN[u] = ch.c[kCN][c]; cA[u] = ch.c[kCA][c];
+            }
           }
-          if (R & bit) {
-            const int Pr = cP + __popc(R & lm);
-            const unsigned int hle = H & (lm | bit), hgt = H & ~(lm | bit);
-            const int M = hle ? cP + __popc(R & lowmask(31 - __clz(hle))) : cM;
-            int N = hgt ? cP + __popc(R & lowmask(__ffs(hgt) - 1)) : cN;
+#pragma unroll
+          for (int u = 0; u < UN; ++u) {
+            if (!(R[u] & bit)) continue;
+            const int Pr = cP[u] + __popc(R[u] & lm);
+            const unsigned int hle = H[u] & (lm | bit), hgt = H[u] & ~(lm | bit);
+            const int M = hle ? cP[u] + __popc(R[u] & lowmask(31 - __clz(hle))) : cM[u];
+            int N = hgt ? cP[u] + __popc(R[u] & lowmask(__ffs(hgt) - 1)) : cN[u];
             if (N > S1) N = S1;
-            const bool tsplit = (T & bit) != 0;
+            const bool tsplit = (T[u] & bit) != 0;
             const uint8_t hd = Pr == M ? kHead : 0;
-            const int i = c * 32 + lane;
+            const int i = (c0 + u * CS) * 32 + lane;
             int rl, ru = -1;
             if (tsplit) {
               rl = (M - S0) + (Pr - S0);
               ru = (N - S0) + (Pr - S0);
             } else {
-              rl = cA + __popc(R & lm) + __popc(U & lm) - A0;
-              if (U & bit) ru = rl + 1;
+              rl = cA[u] + __popc(R[u] & lm) + __popc(U[u] & lm) - A0;
+              if (U[u] & bit) ru = rl + 1;
             }
             outr[base + rl] = (unsigned)i;
             fln[base + rl] = hd;
@@ -1079,8 +1080,6 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
               fln[base + ru] = tsplit ? hd : 0;
             }
           }
-          R = R2; H = H2; T = T2; U = U2;
-          cP = cP2; cM = cM2; cN = cN2; cA = cA2;
         }
       } else
       for (int i = tid; i < n; i += NT) {
