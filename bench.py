@@ -227,9 +227,20 @@ def main():
         kw = dict(delta=torch.from_numpy(w.delta).to(dev), max_checks=torch.from_numpy(w.max_checks).to(dev))
     stream = torch.cuda.current_stream(dev)
 
+    # the library solves a batch in 2^22-query chunks and records its stage
+    # events once per chunk; a multi-chunk step is issued chunk by chunk here
+    # (the same kernels on the same stream) so that every chunk's stages are
+    # timed and summed
+    CH = 1 << 22
+    nch = (Q + CH - 1) // CH
+
     def step(events=None):
-        return solve_batch(pts, kind, outputs=("status", "toi"), device=dev,
-                           raise_on_error=False, events=events, **kw)
+        for j in range(nch):
+            lo, hi = j * CH, min(Q, (j + 1) * CH)
+            kj = {k: v[lo:hi] for k, v in kw.items()}
+            solve_batch(pts[lo:hi], kind[lo:hi], outputs=("status", "toi"), device=dev,
+                        raise_on_error=False,
+                        events=events[4 * j:4 * j + 4] if events else None, **kj)
 
     # untimed: full outputs once, for the algorithmic work (checks) and hits
     full = solve_batch(pts, kind, device=dev, stats=True, **kw)
@@ -250,7 +261,8 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # per step: solve start + the library's 4 stage events (prologue, light,
     # medium, giant done), all on the launching stream; handles created here
-    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(1 + 4 * nch)]
+           for _ in range(args.steps)]
     for row in sev:
         for ev in row:
             ev.record(stream)
@@ -264,7 +276,9 @@ def main():
     barrier()
     ms = e0.elapsed_time(e1) / args.steps
     stage_names = ("prologue", "light", "medium", "giant")
-    stage_ms = {nm: statistics.mean(sev[k][j].elapsed_time(sev[k][j + 1]) for k in range(args.steps))
+    # stage j of chunk c runs from event 4c + j to 4c + j + 1 (event 0: step start)
+    stage_ms = {nm: statistics.mean(sum(sev[k][4 * c + j].elapsed_time(sev[k][4 * c + j + 1])
+                                        for c in range(nch)) for k in range(args.steps))
                 for j, nm in enumerate(stage_names)}
     # end to end through the public API with pinned host buffers
     barrier()

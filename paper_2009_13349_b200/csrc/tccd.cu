@@ -12,11 +12,13 @@
 //  2. engine_kernel tiers (tccd_engine.cuh), each a persistent grid whose
 //     independent groups keep several queries resident and advance them one
 //     BFS level per round with lane-per-box classification:
-//        light  : 256-thread CTA, 64 queries, levels <= 1024 boxes,
-//                 per-box bookkeeping in shared memory
-//        medium : 512-thread CTA, 16 queries, levels <= 32768 boxes
+//        light  : 128-thread CTA (5 per SM), 32 queries, levels <= 1024
+//                 boxes, per-box bookkeeping in shared memory
+//        medium : 256-thread CTA (2 per SM), 8 queries, levels <= 8192
+//                 boxes, per-box bookkeeping in shared memory
 //        giant  : 512-thread CTA per query, levels up to 2 * m_I boxes
-//     A query whose level outgrows its tier restarts in the next tier.
+//     A query whose level outgrows its tier moves to the next tier with its
+//     next level handed over (or restarts there if the handover pool is full).
 //
 // The host splits large batches into chunks (bounded queue memory).
 #include <cuda_runtime.h>
@@ -281,10 +283,10 @@ namespace tccd {
 using LightCfg = EngineCfg<TCCD_LNT, TCCD_LNT, TCCD_LQ, TCCD_LCAP, TCCD_LQCAP, TCCD_LADMIT, true,
                            TCCD_LMINB>;
 #ifndef TCCD_MNT
-#define TCCD_MNT 512
+#define TCCD_MNT 256
 #endif
 #ifndef TCCD_MQ
-#define TCCD_MQ 16
+#define TCCD_MQ 8
 #endif
 #ifndef TCCD_MCAP
 #define TCCD_MCAP 16384
@@ -293,7 +295,7 @@ using LightCfg = EngineCfg<TCCD_LNT, TCCD_LNT, TCCD_LQ, TCCD_LCAP, TCCD_LQCAP, T
 #define TCCD_MADMIT 8192
 #endif
 #ifndef TCCD_MMINB
-#define TCCD_MMINB 1
+#define TCCD_MMINB 2
 #endif
 #if TCCD_MSMEM
 using MediumCfg = EngineCfg<TCCD_MNT, TCCD_MNT, TCCD_MQ, TCCD_MCAP, 8192, TCCD_MADMIT, true,
