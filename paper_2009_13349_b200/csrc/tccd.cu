@@ -303,7 +303,13 @@ using MediumCfg = EngineCfg<TCCD_MNT, TCCD_MNT, TCCD_MQ, TCCD_MCAP, 8192, TCCD_M
 #else
 using MediumCfg = EngineCfg<512, 512, 16, 65536, 32768, 16384, false, 1>;
 #endif
-using GiantCfg = EngineCfg<512, 512, 1, 0, 0, 0, false, 1>;
+#ifndef TCCD_GNT
+#define TCCD_GNT 512
+#endif
+#ifndef TCCD_GMINB
+#define TCCD_GMINB 1
+#endif
+using GiantCfg = EngineCfg<TCCD_GNT, TCCD_GNT, 1, 0, 0, 0, false, TCCD_GMINB>;
 
 template <class Cfg>
 constexpr int groups_per_cta() { return Cfg::NT / Cfg::G; }

@@ -20,6 +20,7 @@ ap.add_argument("--start", type=int, default=0)
 ap.add_argument("--sep", type=float, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--heavy-only", action="store_true")
+ap.add_argument("--heavy-blocks", type=int, default=None)
 args = ap.parse_args()
 w = W.generate(args.config, args.start, args.queries, separation=args.sep)
 dev = torch.device("cuda", 0)
@@ -34,6 +35,7 @@ for r in range(args.reps):
     e0.record()
     out = solve_batch(pts, kind, outputs=("status", "toi", "checks"), device=dev,
                       separation=w.separation, heavy_only=args.heavy_only, stats=True,
+                      heavy_blocks=args.heavy_blocks,
                       events=ev, **kw)
     e1.record()
     torch.cuda.synchronize()
