@@ -29,11 +29,16 @@ _IRF_FIELDS = ("status", "toi", "tol", "codom", "checks", "early", "witness", "l
 
 
 def irf_batch(points, kind, delta=1e-6, max_checks=1_000_000, t_max=1.0, *, device=None,
-              big_slots: int | None = None, raise_on_error: bool = True) -> dict:
+              big_slots: int | None = None, raise_on_error: bool = True,
+              heavy_only: bool = False) -> dict:
     """Interval root finding for a batch ([n, 8, 3] f64 points, kind [n] or
     scalar; delta / max_checks / t_max scalars or [n]).  Returns the solver's
     output dict (status, toi = +inf when free, tol, codom, checks, early,
-    witness, level); host inputs give host outputs."""
+    witness, level); host inputs give host outputs.
+
+    heavy_only=True sends every query through the warp-per-query run search
+    (pass 2 of csrc/irf.cu) instead of only those whose heap outgrows the
+    thread-per-query first pass (tests; same results)."""
     host_in = not (isinstance(points, torch.Tensor) and points.is_cuda)
     dev = torch.device(device) if device is not None else (
         points.device if not host_in else torch.device("cuda", torch.cuda.current_device()))
@@ -69,6 +74,7 @@ def irf_batch(points, kind, delta=1e-6, max_checks=1_000_000, t_max=1.0, *, devi
         ws = _workspace(dev, nbytes)
         b = _lib.TccdBatch()
         b.struct_size = ctypes.sizeof(_lib.TccdBatch)
+        b.flags = _lib.FLAG_HEAVY_ONLY if heavy_only else 0
         b.n = n
         b.points = _ptr(pts)
         b.kind = _ptr(kind_t)

@@ -34,6 +34,38 @@ def test_gpu_irf_matches_reference(cuda, name):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", IRF_SETS)
+def test_gpu_irf_run_search_matches_reference(cuda, name):
+    """Every query through pass 2 (warp per query over runs of equal
+    (t_lo, level)), against the reference's own outputs."""
+    from paper_2009_13349_b200.baselines import irf_batch
+    g = load_golden(name)
+    got = irf_batch(torch.from_numpy(g["points"]), torch.from_numpy(g["kind"]),
+                    torch.from_numpy(g["delta"]), torch.from_numpy(g["max_checks"]),
+                    torch.from_numpy(g["t_max"]), device=cuda, raise_on_error=False,
+                    heavy_only=True)
+    assert_same_results({k: v.numpy() for k, v in got.items()}, g, name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,start,count,kw", [
+    (0, 10_000, 2_000, dict(max_checks=20_000)),
+    (3, 50_000, 2_000, dict(max_checks=20_000)),
+    (2, 1_000, 300, dict(max_checks=20_000)),
+    (0, 30_000, 1_000, dict(max_checks=10_000, t_max=0.7, delta=1e-4)),
+])
+def test_gpu_irf_run_search_vs_oracle(cuda, config, start, count, kw):
+    from paper_2009_13349_b200 import workloads as W
+    from paper_2009_13349_b200.baselines import irf_batch
+    w = W.generate(config, start, count)
+    d, mc, tm = kw.get("delta", 1e-6), kw["max_checks"], kw.get("t_max", 1.0)
+    ref = oracle.irf_batch(w.points, w.kind, d, mc, tm)
+    got = irf_batch(torch.from_numpy(w.points), torch.from_numpy(w.kind), d, mc, tm, device=cuda,
+                    heavy_only=True)
+    assert_same_results({k: v.numpy() for k, v in got.items()}, ref, f"irf runs c{config}")
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("config,start,count,kw", [
     (0, 10_000, 4_000, dict(max_checks=5_000)),
     (3, 50_000, 8_000, dict(max_checks=5_000)),

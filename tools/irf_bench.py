@@ -62,9 +62,10 @@ def main():
         # CPU: the oracle IRF on consecutive chunks until cpu-seconds elapsed
         import oracle
         threads = len(os.sched_getaffinity(0))
-        done, t_cpu, lo = 0, 0.0, 0
+        done, t_cpu, lo, step = 0, 0.0, 0, 32
         while t_cpu < args.cpu_seconds and lo < args.queries:
-            n = min(20_000, args.queries - lo)
+            n = min(step, args.queries - lo)
+            step = min(2 * step, 20_000)  # (heavy workloads: small first chunks)
             t0 = time.perf_counter()
             oracle.irf_batch(w.points[lo:lo + n], w.kind[lo:lo + n], 1e-6, args.max_checks, 1.0,
                              threads=threads)
