@@ -699,11 +699,28 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           b = p;
           if ((f & kClassified) && (f & 3) != kDisjoint) wb = wbp[src];
         } else {
-          double mid;
-          const int sdim = split_dim(p, qp.kap, mid);
-          Box c0, c1;
-          children(p, sdim, mid, c0, c1);
-          b = (r & kRefCb) ? c1 : c0;
+          // the parent's split: its dimension is in its flag byte (shared-
+          // memory tiers; the global tier recomputes it rather than wait on
+          // a dependent global load), the midpoint is recomputed exactly
+          int sdim;
+          if constexpr (Cfg::SMEM) {
+            sdim = (pick(flags, prv)[src] >> 3) & 3;
+          } else {
+            double m_;
+            sdim = split_dim(p, qp.kap, m_);
+          }
+          const bool up = (r & kRefCb) != 0;
+          b = p;
+          if (sdim == 0) {
+            const double mid = 0.5 * (p.t0 + p.t1);
+            if (up) b.t0 = mid; else b.t1 = mid;
+          } else if (sdim == 1) {
+            const double mid = 0.5 * (p.u0 + p.u1);
+            if (up) b.u0 = mid; else b.u1 = mid;
+          } else {
+            const double mid = 0.5 * (p.v0 + p.v1);
+            if (up) b.v0 = mid; else b.v1 = mid;
+          }
         }
       }
       const int k = i - S.seg_off[s];
