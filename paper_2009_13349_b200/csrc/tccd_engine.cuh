@@ -659,8 +659,15 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     boxes += (unsigned long long)n1;
     unsigned int r_cur = tid < n1 ? rf[tid] : kRefRoot;
     Box p_cur;
-    if (!(r_cur & kRefRoot)) p_cur = bprev[r_cur & kRefSrcMask];
-    else if ((r_cur & kRefExt) == kRefExt) p_cur = pool[r_cur & kRefSrcMask];
+    // (global tier: the parent's flag byte travels with the parent box)
+    const uint8_t* const flp = pick(flags, prv);
+    uint8_t pf_cur = 0;
+    if (!(r_cur & kRefRoot)) {
+      p_cur = bprev[r_cur & kRefSrcMask];
+      if constexpr (!Cfg::SMEM) pf_cur = flp[r_cur & kRefSrcMask];
+    } else if ((r_cur & kRefExt) == kRefExt) {
+      p_cur = pool[r_cur & kRefSrcMask];
+    }
     unsigned int r_nxt = tid + NT < n1 ? rf[tid + NT] : kRefRoot;
     // (global flags: prefetched one iteration ahead as well)
     uint8_t f_cur = 0;
@@ -673,11 +680,18 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         f_cur = i + NT < n1 ? fl[i + NT] : 0;
       }
       Box p_nxt;
-      if (!(r_nxt & kRefRoot)) p_nxt = bprev[r_nxt & kRefSrcMask];
-      else if ((r_nxt & kRefExt) == kRefExt) p_nxt = pool[r_nxt & kRefSrcMask];
+      uint8_t pf_nxt = 0;
+      if (!(r_nxt & kRefRoot)) {
+        p_nxt = bprev[r_nxt & kRefSrcMask];
+        if constexpr (!Cfg::SMEM) pf_nxt = flp[r_nxt & kRefSrcMask];
+      } else if ((r_nxt & kRefExt) == kRefExt) {
+        p_nxt = pool[r_nxt & kRefSrcMask];
+      }
       const unsigned int r_nn = i + 2 * NT < n1 ? rf[i + 2 * NT] : kRefRoot;
       const unsigned int r = r_cur;
       const Box p = p_cur;
+      const uint8_t pf = pf_cur;
+      pf_cur = pf_nxt;
       r_cur = r_nxt;
       p_cur = p_nxt;
       r_nxt = r_nn;
@@ -699,16 +713,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           b = p;
           if ((f & kClassified) && (f & 3) != kDisjoint) wb = wbp[src];
         } else {
-          // the parent's split: its dimension is in its flag byte (shared-
-          // memory tiers; the global tier recomputes it rather than wait on
-          // a dependent global load), the midpoint is recomputed exactly
-          int sdim;
-          if constexpr (Cfg::SMEM) {
-            sdim = (pick(flags, prv)[src] >> 3) & 3;
-          } else {
-            double m_;
-            sdim = split_dim(p, qp.kap, m_);
-          }
+          // the parent's split: its dimension is in its flag byte (loaded
+          // with the parent box in the global tier), the midpoint is
+          // recomputed exactly
+          const int sdim = ((Cfg::SMEM ? flp[src] : pf) >> 3) & 3;
           const bool up = (r & kRefCb) != 0;
           b = p;
           if (sdim == 0) {
