@@ -280,7 +280,10 @@ namespace tccd {
 #ifndef TCCD_LMINB
 #define TCCD_LMINB 5
 #endif
-using LightCfg = EngineCfg<TCCD_LNT, TCCD_LNT, TCCD_LQ, TCCD_LCAP, TCCD_LQCAP, TCCD_LADMIT, true,
+#ifndef TCCD_LG
+#define TCCD_LG TCCD_LNT
+#endif
+using LightCfg = EngineCfg<TCCD_LG, TCCD_LNT, TCCD_LQ, TCCD_LCAP, TCCD_LQCAP, TCCD_LADMIT, true,
                            TCCD_LMINB>;
 #ifndef TCCD_MNT
 #define TCCD_MNT 256
