@@ -41,6 +41,20 @@
 namespace tccd {
 
 constexpr int kIntMax = 0x7fffffff;
+
+// Bounds checks of a diagnostic build (-DTCCD_CHECKS): a violated index
+// traps the kernel (the launch fails with an error) instead of corrupting
+// memory.  Compiled out otherwise.
+#ifdef TCCD_CHECKS
+#define TCCD_ASSERT(c) \
+  do {                 \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define TCCD_ASSERT(c) \
+  do {                 \
+  } while (0)
+#endif
 constexpr uint8_t kClassified = 64;  // flag bit: box already classified
 constexpr uint8_t kHead = 128;       // flag bit: first box of a run of equal t_lo
 
@@ -614,12 +628,14 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       if (tid == 0) { S.seg_off[s] = pos; S.seg_n[s] = nr; }
       if (off < 0) {
         if (tid == 0) {
+          TCCD_ASSERT(pos < cap);
           pick(ar.ref, cur)[pos] = kRefRoot;
           pick(slot_of, cur)[pos] = (uint8_t)s;
           pick(flags, cur)[pos] = S.root_flag[s] | kHead;
         }
       } else {
         for (int b = tid; b < nr; b += NT) {
+          TCCD_ASSERT(pos + b < cap && off + b < io.pool_cap);
           pick(ar.ref, cur)[pos + b] = kRefExt | (unsigned)(off + b);
           pick(slot_of, cur)[pos + b] = (uint8_t)s;
           pick(flags, cur)[pos + b] = io.in_pflag[off + b];
@@ -638,6 +654,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     TCCD_PHASE(1);
     TCCD_PHASE(2);
     const int n = S.n_cur;
+    TCCD_ASSERT(n <= cap);
     if (n == 0) break;
     ++rounds;
     Box* const bx = pick(ar.box, cur);
@@ -1098,6 +1115,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
               rl = cA[u] + __popc(R[u] & lm) + __popc(U[u] & lm) - A0;
               if (U[u] & bit) ru = rl + 1;
             }
+            TCCD_ASSERT(base + rl < cap && base + ru < cap);
             outr[base + rl] = (unsigned)i;
             fln[base + rl] = hd;
             if (ru >= 0) {
@@ -1123,6 +1141,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         if (cs == 0) continue;
         if (cs == 2) {
           const int pos = S.next_off[s] + (i - S.seg_off[s]);
+          TCCD_ASSERT(pos < cap);
           outr[pos] = (unsigned)i | kRefSelf;
           sln[pos] = (uint8_t)s;
           fln[pos] = fl[i];
@@ -1156,6 +1175,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         const uint8_t hu = tsplit ? hd : 0;
         if (!hand) {
           const int base = S.next_off[s];
+          TCCD_ASSERT(base + rl < cap && base + ru < cap);
           outr[base + rl] = (unsigned)i;
           sln[base + rl] = (uint8_t)s;
           fln[base + rl] = hd;
@@ -1172,6 +1192,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           const int sd = split_dim(pb, S.qp[s].kap, mid);
           Box c0, c1;
           children(pb, sd, mid, c0, c1);
+          TCCD_ASSERT(base + rl < io.pool_cap && base + ru < io.pool_cap);
           io.out_pbox[base + rl] = c0;
           io.out_pflag[base + rl] = hd;
           if (ru >= 0) {
@@ -1199,6 +1220,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       const unsigned int ob = (unsigned)(ch.c[kCB][c] + __popc(ch.m[kMT][c] & lm));
       const unsigned int push = oa + ob;
       const unsigned long long k0 = tkey(b.t0);
+      TCCD_ASSERT(oa + 1 < 2 * cap && ob < cap);
       ar.akey[oa] = k0;
       ar.apush[oa] = push;
       ar.aref[oa] = (unsigned)i;
@@ -1271,6 +1293,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         }
         if (!hand) {
           const int pos = S.next_off[s] + rank;
+          TCCD_ASSERT(pos < cap);
           out[pos] = r;
           sln[pos] = (uint8_t)s;
           fln[pos] = 0;
@@ -1280,6 +1303,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           const int sd = split_dim(pb, S.qp[s].kap, mid);
           Box c0, c1;
           children(pb, sd, mid, c0, c1);
+          TCCD_ASSERT(S.hoff[s] + rank < io.pool_cap);
           io.out_pbox[S.hoff[s] + rank] = (r & kRefCb) ? c1 : c0;
           io.out_pflag[S.hoff[s] + rank] = 0;
         }
