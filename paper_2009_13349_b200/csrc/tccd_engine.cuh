@@ -859,7 +859,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       }
       if (done) S.qidx[s] = -1;
     }
-    gsync<G>();
+    // (P4 reads only P1's chunk masks, so it needs no barrier after P3; the
+    // one-query tiers read P3's outcome below)
+    if constexpr (ONEQ) gsync<G>();
     TCCD_PHASE(4);
     const int nxt = prv;
     // one query that ended this round: no next level to build
