@@ -328,6 +328,38 @@ __global__ void stats_kernel(Args a, int heavy_only) {
   }
 }
 
+// Admission order of the giant tier's queue: largest handed-over level
+// first (longest-processing-time-first, so the heaviest queries do not start
+// last and leave the other SMs idle).  Only a scheduling order: every query's
+// result is independent of it.  Queues above kOrderMax keep their order.
+constexpr int kOrderMax = 4096;
+__global__ void __launch_bounds__(1024) order_kernel(const Hand* hand,
+                                                     const unsigned long long* count,
+                                                     unsigned int* perm) {
+  __shared__ unsigned long long key[kOrderMax];
+  const unsigned long long n = *count;
+  if (n < 2 || n > (unsigned long long)kOrderMax) return;
+  int P = 2;
+  while (P < (int)n) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    const unsigned int w = i < (int)n && hand[i].n > 0 ? (unsigned int)hand[i].n : 0u;
+    key[i] = i < (int)n ? ((unsigned long long)(0xffffffffu - w) << 32) | (unsigned int)i : ~0ull;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long a = key[i], b = key[l];
+          if (((i & k) == 0) == (a > b)) { key[i] = b; key[l] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < (int)n; i += blockDim.x) perm[i] = (unsigned int)(key[i] & 0xffffffffu);
+}
+
 }  // namespace tccd
 
 // ===========================================================================
@@ -352,7 +384,7 @@ long long giant_cap(long long mcmax) { return 2 * mcmax + 2; }
 constexpr long long kPool = 1LL << 24;  // handover pool boxes per tier transition
 
 struct Layout {
-  size_t ctr, queue[3], hand[3], pbox[3], pflag[3], light, medium, giant, total;
+  size_t ctr, queue[3], hand[3], pbox[3], pflag[3], perm, light, medium, giant, total;
   size_t light_b, medium_b, giant_b;
   int light_blocks, medium_blocks, giant_blocks;
 };
@@ -375,6 +407,7 @@ Layout layout(long long n, long long mcmax, int giant_blocks, int sms) {
     L.pbox[k] = o; o += align256((size_t)kPool * sizeof(Box));
     L.pflag[k] = o; o += align256((size_t)kPool);
   }
+  L.perm = o; o += align256((size_t)kOrderMax * 4);
   L.light = o; o += L.light_b * (size_t)L.light_blocks * groups_per_cta<LightCfg>();
   L.medium = o; o += L.medium_b * (size_t)L.medium_blocks * groups_per_cta<MediumCfg>();
   L.giant = o; o += L.giant_b * (size_t)L.giant_blocks;
@@ -492,6 +525,8 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
     io.in_pbox = tier > 0 ? (const Box*)(ws + L.pbox[tier]) : nullptr;
     io.in_pflag = tier > 0 ? (const uint8_t*)(ws + L.pflag[tier]) : nullptr;
     io.in_maxsz = tier == 0 ? 1 : 2 * (tier == 1 ? LightCfg::QCAP : MediumCfg::QCAP);
+    io.in_perm = tier == 2 && !a.heavy_only ? (const unsigned int*)(ws + L.perm) : nullptr;
+    io.perm_max = kOrderMax;
     io.out_hand = tier < 2 ? (Hand*)(ws + L.hand[tier + 1]) : nullptr;
     io.out_pbox = tier < 2 ? (Box*)(ws + L.pbox[tier + 1]) : nullptr;
     io.out_pflag = tier < 2 ? (uint8_t*)(ws + L.pflag[tier + 1]) : nullptr;
@@ -539,6 +574,11 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
       if (mark(2) != cudaSuccess) return TCCD_E_CUDA;
     } else if (mark(1) != cudaSuccess || mark(2) != cudaSuccess) {
       return TCCD_E_CUDA;
+    }
+    if (!a.heavy_only) {
+      order_kernel<<<1, 1024, 0, st>>>((const Hand*)(ws + L.hand[2]), &a.ctr->q_count[2],
+                                       (unsigned int*)(ws + L.perm));
+      if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
     }
     if ((rc = launch_tier<GiantCfg>(a, io_for(2), L.giant_blocks, st)) != TCCD_OK) return rc;
     if (mark(3) != cudaSuccess) return TCCD_E_CUDA;

@@ -394,6 +394,8 @@ struct TierIO {
   const Box* in_pbox;       // handover pool the input levels live in
   const uint8_t* in_pflag;
   int in_maxsz;             // largest handed-over level
+  const unsigned int* in_perm;  // admission order of the input queue (nullptr: queue order)
+  long long perm_max;       // in_perm holds an order only for queues up to this size
   Hand* out_hand;           // handover state / pool of the next tier
   Box* out_pbox;
   uint8_t* out_pflag;
@@ -449,6 +451,9 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   const int qcap = Cfg::QCAP ? Cfg::QCAP : cap;
   const int admit_lim = Cfg::ADMIT ? Cfg::ADMIT : cap;
   const unsigned long long in_total = *(volatile unsigned long long*)io.in_count;
+  // queue entry admitted at position k
+  const bool use_perm = io.in_perm && in_total >= 2 && (long long)in_total <= io.perm_max;
+  auto entry = [&](long long k) -> long long { return use_perm ? (long long)io.in_perm[k] : k; };
   const int tid = threadIdx.x % G;  // rank within the group
   for (int s = tid; s < Q; s += NT) S.qidx[s] = -1;
   if (tid == 0) { S.n_cur = 0; S.exhausted = 0; S.rot = 0; S.deferred = 0; S.deferred_last = 0; }
@@ -569,7 +574,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       for (int r = wid; r < k_adm; r += NWARP) {
         const int s = S.adm_slot[r];
         const unsigned long long* src =
-            reinterpret_cast<const unsigned long long*>(io.in + S.admit_base + r);
+            reinterpret_cast<const unsigned long long*>(io.in + entry(S.admit_base + r));
         for (int wd = lane; wd < kPreWords; wd += 32) {
           const unsigned long long v = src[wd];
           if (wd < 24) reinterpret_cast<unsigned long long*>(S.P[s])[wd] = v;
@@ -590,8 +595,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       S.uniform[s] = frexp(S.qp[s].t_max, &ex) == 0.5;  // t_max a power of two
       int nr = 1;
       long long off = -1;
-      if (io.in_hand && io.in_hand[S.admit_base + r].n > 0) {
-        const Hand& hd = io.in_hand[S.admit_base + r];
+      if (io.in_hand && io.in_hand[entry(S.admit_base + r)].n > 0) {
+        const Hand& hd = io.in_hand[entry(S.admit_base + r)];
         nr = hd.n;
         off = hd.off;
         S.C[s] = hd.C;
