@@ -324,12 +324,15 @@ def main():
     dom = max(("light", "medium", "giant"), key=lambda nm: stage_ms[nm])
     achieved = tier_flops[dom] / (stage_ms[dom] * 1e-3) / 1e12
     traffic = None
+    ncu_counters = None
     tpath = os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tj = json.load(fh)
         if tj.get("kernel") == dom and tj.get("config") == args.config and tj.get("queries") == Q:
             traffic = tj["dram_bytes_per_launch"]
+            ncu_counters = {k: tj[k] for k in ("fp64_pipe_active_pct", "warp_execution_efficiency_pct",
+                                               "dram_gbs", "issue_slots_busy_pct") if k in tj}
     cpu = None
     if world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
@@ -364,7 +367,8 @@ def main():
                      "solve_flops_per_step": flops,
                      "solve_achieved_tflops": flops / (ms * 1e-3) / 1e12,
                      "traffic_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum"
-                                       " (profiles/r01/roofline_traffic.json)"},
+                                       " (profiles/r01/roofline_traffic.json)",
+                     "ncu_counters": ncu_counters},
         "cpu_baseline": cpu,
         "clocks": clk,
         "gpu_launches": 2 * args.steps * LAUNCHES_PER_SOLVE * ((Q + (1 << 22) - 1) >> 22),
