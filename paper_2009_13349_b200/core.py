@@ -51,6 +51,17 @@ class Query:
         if not isinstance(self.kind, QueryKind):
             object.__setattr__(self, "kind", QueryKind(self.kind))
 
+    @classmethod
+    def _trusted(cls, kind: QueryKind, points0: tuple, points1: tuple) -> "Query":
+        """A Query from values that already satisfy the checks above (finite
+        float coordinates read back from a validated batch): the same object,
+        without re-validating 24 coordinates one by one."""
+        q = object.__new__(cls)
+        object.__setattr__(q, "kind", kind)
+        object.__setattr__(q, "points0", points0)
+        object.__setattr__(q, "points1", points1)
+        return q
+
     def as_arrays(self) -> tuple[np.ndarray, np.ndarray]:
         return (np.array(self.points0, dtype=np.float64),
                 np.array(self.points1, dtype=np.float64))
@@ -75,6 +86,16 @@ class DomainBox:
                 raise ValueError(f"DomainBox.{name} = ({lo}, {hi}) not nested in [0, 1]")
         if self.level < 0:
             raise ValueError("DomainBox.level must be >= 0")
+
+    @classmethod
+    def _trusted(cls, t: tuple, u: tuple, v: tuple, level: int) -> "DomainBox":
+        """A DomainBox from a solver witness (nested in [0, 1] by construction)."""
+        b = object.__new__(cls)
+        object.__setattr__(b, "t", t)
+        object.__setattr__(b, "u", u)
+        object.__setattr__(b, "v", v)
+        object.__setattr__(b, "level", level)
+        return b
 
     @property
     def widths(self) -> tuple[float, float, float]:

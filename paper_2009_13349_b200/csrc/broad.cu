@@ -393,6 +393,28 @@ int bits_for(long long n) {  // bits to index [0, n)
 
 unsigned nblk(long long n, int t = kT) { return (unsigned)((n + t - 1) / t); }
 
+// The broad phase allocates its temporaries stream-ordered and synchronizes
+// a few times (candidate counts).  With the default pool's release threshold
+// of 0 every synchronization hands the freed blocks back to the driver, and
+// the next allocation maps them again (tens of ms for a million-triangle
+// mesh).  The device's default pool keeps up to this much freed memory
+// instead (set once per device; the caller's own allocator is not affected).
+constexpr unsigned long long kPoolKeep = 4ull << 30;
+
+cudaError_t keep_pool() {
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return e;
+  cudaMemPool_t pool;
+  if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
+  unsigned long long keep = kPoolKeep;
+  if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess)
+    return e;
+  done[dev] = true;
+  return cudaSuccess;
+}
+
 template <class T>
 cudaError_t dalloc(T** p, long long count, cudaStream_t st) {
   return cudaMallocAsync((void**)p, (size_t)(count > 0 ? count : 1) * sizeof(T), st);
@@ -461,6 +483,7 @@ int tccd_broad_create(const tccd_mesh* m, double inflation, tccd_broad** out, in
   if (nv > 0 && (!m->x0 || !m->x1)) return TCCD_E_NULL;
   if ((nt > 0 && !m->triangles) || (ne > 0 && !m->edges)) return TCCD_E_NULL;
   if (nv >= (1ll << 31) || nt >= (1ll << 31) || ne >= (1ll << 31)) return TCCD_E_CAPACITY;
+  if (keep_pool() != cudaSuccess) return TCCD_E_CUDA;
   tccd_broad* h = new tccd_broad;
   memset(h, 0, sizeof(*h));
   h->st = (cudaStream_t)stream;

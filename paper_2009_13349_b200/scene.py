@@ -23,6 +23,8 @@ narrow phase reads them without a host round trip.
 
 from __future__ import annotations
 
+import contextlib
+import gc
 import math
 from dataclasses import dataclass
 from typing import Callable
@@ -139,8 +141,36 @@ class CandidateSet:
                                                                   tuple(map(tuple, p[4:]))))
 
     def to_list(self) -> list:
+        """All candidates as ContactCandidate objects (bulk conversion: the
+        coordinates come from a validated mesh, so the Query objects are
+        built without re-checking them)."""
         h = self.host()
-        return [h.candidate(i) for i in range(h.m)]
+        pts = h.points.tolist()
+        kinds = h.kind.tolist()
+        idx = h.indices.tolist()
+        K = (QueryKind.VERTEX_FACE, QueryKind.EDGE_EDGE)
+        out = []
+        with _bulk():
+            for i in range(h.m):
+                p = pts[i]
+                k = K[kinds[i]]
+                q = Query._trusted(k, (tuple(p[0]), tuple(p[1]), tuple(p[2]), tuple(p[3])),
+                                   (tuple(p[4]), tuple(p[5]), tuple(p[6]), tuple(p[7])))
+                out.append(ContactCandidate(k, (idx[i][0], idx[i][1]), q))
+        return out
+
+
+@contextlib.contextmanager
+def _bulk():
+    """Millions of acyclic result objects: keep the cyclic collector from
+    rescanning them while they are built."""
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        yield
+    finally:
+        if was:
+            gc.enable()
 
 
 def load_obj(path) -> tuple[np.ndarray, np.ndarray]:
@@ -265,9 +295,14 @@ def construct_active_set(mesh: TriMeshPair, delta: float = 1e-6, max_checks: int
     hits, r = active_set_batch(mesh, delta, max_checks, separation, device)
     if hits.m == 0:
         return []
-    hc = hits.host()
-    res = {k: _np(r[k]) for k in ("toi", "witness", "level")}
-    return [(hc.candidate(i), float(res["toi"][i]), _witness(res, i)) for i in range(hc.m)]
+    cands = hits.to_list()
+    toi = _np(r["toi"]).tolist()
+    w = _np(r["witness"]).tolist()
+    lv = _np(r["level"]).tolist()
+    with _bulk():
+        return [(c, toi[i], DomainBox._trusted((w[i][0], w[i][1]), (w[i][2], w[i][3]),
+                                                (w[i][4], w[i][5]), lv[i]))
+                for i, c in enumerate(cands)]
 
 
 # --- start-distance lower bounds: the reference's closed forms (scene.py:335-419),
