@@ -285,11 +285,14 @@ def main():
     torch.cuda.synchronize(dev)
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kw_h = {k: v.cpu() for k, v in kw.items()}
-    # untimed warm-up of this path (creates the API's copy stream and the
-    # pinned result buffers), then the timed steps
-    solve_batch(pts_h, kind_h, outputs=("status", "toi"), device=dev, non_blocking=True,
-                **kw_h)["ready"].synchronize()
+    # untimed warm-up of this path, with as many calls in flight as the timed
+    # loop has (creates the API's copy stream; the caching allocators then
+    # hold the device copies and pinned result buffers of every in-flight
+    # step, so no cudaMalloc / cudaHostAlloc synchronizes the timed region)
+    warm = [solve_batch(pts_h, kind_h, outputs=("status", "toi"), device=dev, non_blocking=True,
+                        **kw_h) for _ in range(args.steps)]
     torch.cuda.synchronize(dev)
+    del warm
     f0.record(stream)
     # the points copies run on the API's side stream, ordered after f0; each
     # solve waits for its copy, so step k+1's copy overlaps step k's solve
