@@ -195,6 +195,17 @@ void tccd_broad_destroy(tccd_broad *h);
 size_t tccd_irf_workspace_bytes(int64_t n, int64_t max_checks_max, int32_t big_slots);
 int tccd_irf_batch(const tccd_batch *batch, void *stream);
 
+/*
+ * Copy `bytes` from device memory to pinned (page-locked) host memory with a
+ * kernel on `stream` instead of a copy-engine transfer (new; no reference
+ * counterpart).  A streaming caller's result copies then do not queue in
+ * front of its next batch's host-to-device copy, which the copy engines
+ * would otherwise serve in submission order.  host_dst must be pinned host
+ * memory (device-accessible through unified addressing); returns
+ * TCCD_E_CUDA if it is not, so the caller can fall back to cudaMemcpyAsync.
+ */
+int tccd_copy_to_host(const void *src, void *host_dst, int64_t bytes, void *stream);
+
 const char *tccd_error_string(int code);
 int tccd_abi_version(void);
 

@@ -88,6 +88,7 @@ EXPORTS = (
     "tccd_broad_create",
     "tccd_broad_emit",
     "tccd_broad_destroy",
+    "tccd_copy_to_host",
     "tccd_irf_workspace_bytes",
     "tccd_irf_batch",
 )
@@ -133,6 +134,8 @@ def lib() -> ctypes.CDLL:
         L.tccd_irf_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32]
         L.tccd_irf_batch.restype = ctypes.c_int
         L.tccd_irf_batch.argtypes = [ctypes.POINTER(TccdBatch), _vp]
+        L.tccd_copy_to_host.restype = ctypes.c_int
+        L.tccd_copy_to_host.argtypes = [_vp, _vp, ctypes.c_int64, _vp]
         v = L.tccd_abi_version()
         if v != ABI_VERSION:
             raise RuntimeError(f"libtccd ABI {v} != expected {ABI_VERSION}")

@@ -328,6 +328,18 @@ __global__ void stats_kernel(Args a, int heavy_only) {
   }
 }
 
+// Device -> mapped pinned host copy as a kernel (tccd_copy_to_host): 16-byte
+// stores when both ends are 16-byte aligned, bytes otherwise.
+__global__ void copy_out_kernel(const unsigned char* src, unsigned char* dst, long long bytes) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const bool vec = (((uintptr_t)src | (uintptr_t)dst) & 15) == 0;
+  const long long n16 = vec ? bytes / 16 : 0;
+  for (long long i = t; i < n16; i += stride)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (long long i = n16 * 16 + t; i < bytes; i += stride) dst[i] = src[i];
+}
+
 // Admission order of the giant tier's queue: largest handed-over level
 // first (longest-processing-time-first, so the heaviest queries do not start
 // last and leave the other SMs idle).  Only a scheduling order: every query's
@@ -439,6 +451,22 @@ int launch_tier(const Args& a, const TierIO& io, int blocks, cudaStream_t st) {
 extern "C" {
 
 int tccd_abi_version(void) { return TCCD_ABI_VERSION; }
+
+int tccd_copy_to_host(const void* src, void* host_dst, int64_t bytes, void* stream) {
+  if (bytes < 0) return TCCD_E_N;
+  if (bytes == 0) return TCCD_OK;
+  if (!src || !host_dst) return TCCD_E_NULL;
+  void* dst = nullptr;
+  if (cudaHostGetDevicePointer(&dst, host_dst, 0) != cudaSuccess || !dst) {
+    cudaGetLastError();  // (clear: the caller falls back to a copy-engine transfer)
+    return TCCD_E_CUDA;
+  }
+  const long long n16 = bytes / 16;
+  const int blocks = (int)min(2LL * device_sm_count(0), max(1LL, (n16 + 255) / 256));
+  copy_out_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      (const unsigned char*)src, (unsigned char*)dst, (long long)bytes);
+  return cudaGetLastError() == cudaSuccess ? TCCD_OK : TCCD_E_CUDA;
+}
 
 const char* tccd_error_string(int code) {
   switch (code) {

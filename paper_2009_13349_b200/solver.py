@@ -24,6 +24,7 @@ OUTPUT_FIELDS = ("status", "toi", "tol", "codom", "checks", "early", "witness", 
 
 _workspaces: dict = {}
 _copy_streams: dict = {}
+_staging: dict = {}  # device -> list of [uint8 tensor, torch.cuda.Event | None]
 
 
 def copy_stream(device: torch.device) -> torch.cuda.Stream:
@@ -34,6 +35,31 @@ def copy_stream(device: torch.device) -> torch.cuda.Stream:
     if cs is None:
         cs = _copy_streams[key] = torch.cuda.Stream(device)
     return cs
+
+
+def _staging_buffer(device: torch.device, nbytes: int) -> list:
+    """A device buffer for a non-blocking host->device copy of the points.
+    Buffers are reused once the solve that last read one has finished (its
+    event), so a stream of calls does not go through the caching allocator
+    (whose growth under many calls in flight can block the host for
+    milliseconds).  Returns the slot [buffer, event]."""
+    key = (device.type, device.index)
+    slots = _staging.setdefault(key, [])
+    for slot in slots:
+        buf, ev = slot
+        if buf.numel() >= nbytes and (ev is None or (ev is not _BUSY and ev.query())):
+            slot[1] = _BUSY
+            return slot
+    # (allocated on the copy stream that writes it: a block the caller's
+    # stream freed a moment ago may still be read there)
+    with torch.cuda.stream(copy_stream(device)):
+        slot = [torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device), _BUSY]
+    if len(slots) < 16:
+        slots.append(slot)
+    return slot
+
+
+_BUSY = object()  # a staging slot handed out whose solve is not enqueued yet
 
 
 def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
@@ -106,6 +132,25 @@ def _param(x, n, dtype, device, name):
     return t.to(device=device, dtype=dtype, non_blocking=True).contiguous(), 0
 
 
+def _params(kind, config, delta, max_checks, separation, t_max, n, dev):
+    """Per-query (device tensor) or broadcast (scalar) kind, delta,
+    max_checks, separation and t_max; unset ones from ``config``."""
+    if isinstance(kind, (int, np.integer, QueryKind)):
+        kind_t, kind_all = None, int(kind)
+    else:
+        kind_t, kind_all = _param(kind, n, torch.uint8, dev, "kind")
+        kind_all = int(kind_all)
+    delta_t, delta_all = _param(config.delta if delta is None else delta, n, torch.float64, dev,
+                                "delta")
+    mc_src = config.max_checks if max_checks is None else max_checks
+    mc_t, mc_all = _param(mc_src, n, torch.int64, dev, "max_checks")
+    sep_src = config.separation if separation is None else separation
+    sep_t, sep_all = _param(sep_src, n, torch.float64, dev, "separation")
+    tm_t, tm_all = _param(config.t_max if t_max is None else t_max, n, torch.float64, dev, "t_max")
+    return (kind_t, kind_all, delta_t, delta_all, mc_t, mc_all, sep_t, sep_all, tm_t, tm_all,
+            mc_src, sep_src)
+
+
 def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
@@ -156,27 +201,28 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
     n = int(pts.shape[0])
     if host_in:
         pts = pts.contiguous().pin_memory() if pts.device.type == "cpu" else pts
+    slot = None
     if host_in and non_blocking:
+        # every host input goes over on the API's copy stream: an engine copy
+        # issued on the launching stream would queue behind the solve already
+        # there and hold back the next call's copies
         compute = torch.cuda.current_stream(dev)
         cs = copy_stream(dev)
+        slot = _staging_buffer(dev, pts.numel() * 8)
         with torch.cuda.stream(cs):
-            pts = pts.to(dev, non_blocking=True).contiguous()
+            dst = slot[0][:pts.numel() * 8].view(torch.float64).view(pts.shape)
+            dst.copy_(pts, non_blocking=True)
+            kind_t, kind_all, delta_t, delta_all, mc_t, mc_all, sep_t, sep_all, tm_t, tm_all, \
+                mc_src, sep_src = _params(kind, config, delta, max_checks, separation, t_max, n, dev)
         compute.wait_stream(cs)
-        pts.record_stream(compute)
+        for t in (dst, kind_t, delta_t, mc_t, sep_t, tm_t):
+            if t is not None:
+                t.record_stream(compute)  # (allocated on the copy stream, read by the solve)
+        pts = dst
     else:
         pts = pts.to(dev, non_blocking=True).contiguous()
-
-    if isinstance(kind, (int, np.integer, QueryKind)):
-        kind_t, kind_all = None, int(kind)
-    else:
-        kind_t, kind_all = _param(kind, n, torch.uint8, dev, "kind")
-        kind_all = int(kind_all)
-    delta_t, delta_all = _param(config.delta if delta is None else delta, n, torch.float64, dev, "delta")
-    mc_src = config.max_checks if max_checks is None else max_checks
-    mc_t, mc_all = _param(mc_src, n, torch.int64, dev, "max_checks")
-    sep_src = config.separation if separation is None else separation
-    sep_t, sep_all = _param(sep_src, n, torch.float64, dev, "separation")
-    tm_t, tm_all = _param(config.t_max if t_max is None else t_max, n, torch.float64, dev, "t_max")
+        kind_t, kind_all, delta_t, delta_all, mc_t, mc_all, sep_t, sep_all, tm_t, tm_all, \
+            mc_src, sep_src = _params(kind, config, delta, max_checks, separation, t_max, n, dev)
     if mc_t is not None:
         mc_max = int(torch.as_tensor(mc_src).max().item()) if n else 1
     else:
@@ -252,12 +298,29 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
         stream = torch.cuda.current_stream(dev)
         rc = lib.tccd_solve_batch(ctypes.byref(b), ctypes.c_void_p(stream.cuda_stream))
         _raise_abi(rc, delta_all, mc_all, tm_all, sep_all, kind_all)
-    if host_in:
+    if host_in and non_blocking:
+        # results into pinned host tensors by a copy kernel on the launching
+        # stream, not the copy engines: engine copies are served in submission
+        # order, so a result copy queued behind this solve would hold back the
+        # next call's point copy (and the overlap of copies with solves)
+        stream = torch.cuda.current_stream(dev)
+        hout = {}
+        for k, v in out.items():
+            h = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+            if v.numel() and lib.tccd_copy_to_host(_ptr(v), _ptr(h), v.numel() * v.element_size(),
+                                                   ctypes.c_void_p(stream.cuda_stream)) != 0:
+                h.copy_(v, non_blocking=True)  # (not device-accessible: an engine copy)
+            hout[k] = h
+        out = hout
+    elif host_in:
         out = {k: v.to("cpu", non_blocking=True) for k, v in out.items()}
+    if host_in:
         if non_blocking:
             ready = torch.cuda.Event()
             ready.record(torch.cuda.current_stream(dev))
             out["ready"] = ready
+            if slot is not None:
+                slot[1] = ready  # the staging buffer is free once this solve is done
             if st is not None:
                 out["stats"] = st
             return out
