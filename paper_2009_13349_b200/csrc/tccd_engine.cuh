@@ -724,33 +724,33 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       Box b;
       f = Cfg::SMEM ? fl[i] : f_pre;  // head bit (+ class, for roots and deferred boxes)
       double wb = 0.0;
-      if ((r & kRefExt) == kRefExt) {
-        b = p;  // handed over (unclassified)
-      } else if (r & kRefRoot) {
-        b = Box{0.0, qp.t_max, 0.0, 1.0, 0.0, 1.0};
-        wb = S.root_wb[s];
+      // every kind of box but the root starts from the loaded box p: handed
+      // over (unclassified), deferred (itself, class carried) or a child
+      // (p with one bound replaced by the parent's midpoint)
+      b = p;
+      if (r & kRefRoot) {
+        if ((r & kRefExt) != kRefExt) {
+          b = Box{0.0, qp.t_max, 0.0, 1.0, 0.0, 1.0};
+          wb = S.root_wb[s];
+        }
+      } else if (r & kRefSelf) {
+        if ((f & kClassified) && (f & 3) != kDisjoint) wb = wbp[r & kRefSrcMask];
       } else {
+        // the parent's split: its dimension is in its flag byte (loaded with
+        // the parent box in the global tier), the midpoint is recomputed
+        // exactly
         const int src = (int)(r & kRefSrcMask);
-        if (r & kRefSelf) {
-          b = p;
-          if ((f & kClassified) && (f & 3) != kDisjoint) wb = wbp[src];
+        const int sdim = ((Cfg::SMEM ? flp[src] : pf) >> 3) & 3;
+        const bool up = (r & kRefCb) != 0;
+        if (sdim == 0) {
+          const double mid = 0.5 * (p.t0 + p.t1);
+          if (up) b.t0 = mid; else b.t1 = mid;
+        } else if (sdim == 1) {
+          const double mid = 0.5 * (p.u0 + p.u1);
+          if (up) b.u0 = mid; else b.u1 = mid;
         } else {
-          // the parent's split: its dimension is in its flag byte (loaded
-          // with the parent box in the global tier), the midpoint is
-          // recomputed exactly
-          const int sdim = ((Cfg::SMEM ? flp[src] : pf) >> 3) & 3;
-          const bool up = (r & kRefCb) != 0;
-          b = p;
-          if (sdim == 0) {
-            const double mid = 0.5 * (p.t0 + p.t1);
-            if (up) b.t0 = mid; else b.t1 = mid;
-          } else if (sdim == 1) {
-            const double mid = 0.5 * (p.u0 + p.u1);
-            if (up) b.u0 = mid; else b.u1 = mid;
-          } else {
-            const double mid = 0.5 * (p.v0 + p.v1);
-            if (up) b.v0 = mid; else b.v1 = mid;
-          }
+          const double mid = 0.5 * (p.v0 + p.v1);
+          if (up) b.v0 = mid; else b.v1 = mid;
         }
       }
       const int k = i - S.seg_off[s];
