@@ -1,69 +1,128 @@
-"""Per-step breakdown of the end-to-end (host buffers) solve: H2D copy alone,
-device-resident solve, and the host-input solve through the public API.
+"""Host-side cost of one non-blocking solve_batch call with pinned host
+inputs (the e2e path of bench.py): per-call wall time of the Python API and
+its cProfile breakdown.
 
-    python tools/e2e_probe.py [--config 1] [--queries 1000000] [--steps 6]
+    python tools/e2e_probe.py [--config 0] [--steps 20]
 """
 import argparse
+import cProfile
 import os
+import pstats
 import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2009_13349_b200 import solve_batch, solver  # noqa: E402
+from paper_2009_13349_b200 import solve_batch  # noqa: E402
 from paper_2009_13349_b200 import workloads as W  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--config", type=int, default=1)
+ap.add_argument("--config", type=int, default=0)
 ap.add_argument("--queries", type=int, default=1_000_000)
-ap.add_argument("--steps", type=int, default=6)
+ap.add_argument("--steps", type=int, default=20)
 args = ap.parse_args()
-w = W.generate(args.config, 0, args.queries)
 dev = torch.device("cuda", 0)
+w = W.generate(args.config, 0, args.queries)
 pts_h = torch.from_numpy(w.points).pin_memory()
 kind_h = torch.from_numpy(w.kind).pin_memory()
-pts = pts_h.to(dev)
-kind = kind_h.to(dev)
-s = torch.cuda.current_stream(dev)
 
 
-def timed(fn):
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+def loop():
+    t = []
+    res = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        res.append(solve_batch(pts_h, kind_h, outputs=("status", "toi"), device=dev,
+                               non_blocking=True))
+        t.append(time.perf_counter() - t0)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    a.record(s)
-    fn()
-    b.record(s)
-    torch.cuda.synchronize()
-    return a.elapsed_time(b), 1e3 * (time.perf_counter() - t0)
+    return t
 
 
-solve_batch(pts, kind, outputs=("status", "toi"), device=dev)
+loop()
+t0 = time.perf_counter()
+t = loop()
+wall = time.perf_counter() - t0
+print(f"per call host ms: {[round(1e3 * x, 2) for x in t]}; wall per step {1e3 * wall / args.steps:.2f} ms")
+pr = cProfile.Profile()
+pr.enable()
+loop()
+pr.disable()
+pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
+
+# components: copies alone on the API's copy stream, solves alone (device inputs)
+from paper_2009_13349_b200 import solver  # noqa: E402
+cs = solver.copy_stream(dev)
+bufs = [torch.empty_like(pts_h, device=dev) for _ in range(2)]
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+with torch.cuda.stream(cs):
+    e0.record(cs)
+    for k in range(args.steps):
+        bufs[k % 2].copy_(pts_h, non_blocking=True)
+    e1.record(cs)
+torch.cuda.synchronize()
+print(f"copies alone: {e0.elapsed_time(e1) / args.steps:.2f} ms per step")
+pts_d, kind_d = pts_h.to(dev), kind_h.to(dev)
+solve_batch(pts_d, kind_d, outputs=("status", "toi"), device=dev)
+torch.cuda.synchronize()
+e0.record()
 for k in range(args.steps):
-    h2d = timed(lambda: pts_h.to(dev, non_blocking=True))
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-    dev_solve = timed(lambda: (evs[0].record(s), solve_batch(pts, kind, outputs=("status", "toi"),
-                                                             device=dev, events=evs[1:])))
-    stages = [evs[j].elapsed_time(evs[j + 1]) for j in range(4)]
-    host_solve = timed(lambda: solve_batch(pts_h, kind_h, outputs=("status", "toi"), device=dev))
-    ws = solver._workspaces.get(("cuda", 0))
-    hb = solver.default_heavy_blocks(dev, args.queries, 1_000_000)
-    print(f"  heavy_blocks {hb}, workspace {ws.numel() / 2**30:.2f} GiB, "
-          f"free {torch.cuda.mem_get_info(dev)[0] / 2**30:.1f} GiB")
-    print("  stages prologue/light/medium/giant ms: " + " / ".join(f"{x:.2f}" for x in stages))
-    print(f"step {k}: h2d {h2d[0]:.2f} ms ({193e-3 * args.queries / 1e3 / h2d[0]:.1f} GB/s), "
-          f"device solve {dev_solve[0]:.2f} ms, host-input solve {host_solve[0]:.2f} ms "
-          f"(wall {host_solve[1]:.2f})", flush=True)
-
-# host-side cost of the pieces solve_batch runs before its launches
-for k in range(5):
-    t0 = time.perf_counter()
-    torch.cuda.mem_get_info(dev)
-    t1 = time.perf_counter()
-    solver.default_heavy_blocks(dev, args.queries, 1_000_000)
-    t2 = time.perf_counter()
-    solver.sm_count(dev)
-    t3 = time.perf_counter()
-    print(f"mem_get_info {1e3 * (t1 - t0):.3f} ms, default_heavy_blocks {1e3 * (t2 - t1):.3f} ms, "
-          f"sm_count {1e3 * (t3 - t2):.3f} ms")
+    solve_batch(pts_d, kind_d, outputs=("status", "toi"), device=dev)
+e1.record()
+torch.cuda.synchronize()
+print(f"solves alone: {e0.elapsed_time(e1) / args.steps:.2f} ms per step")
+# copies on cs concurrently with solves on the current stream
+e0.record()
+cs.wait_event(e0)
+with torch.cuda.stream(cs):
+    for k in range(args.steps):
+        bufs[k % 2].copy_(pts_h, non_blocking=True)
+for k in range(args.steps):
+    solve_batch(pts_d, kind_d, outputs=("status", "toi"), device=dev)
+torch.cuda.current_stream().wait_stream(cs)
+e1.record()
+torch.cuda.synchronize()
+print(f"copies || solves: {e0.elapsed_time(e1) / args.steps:.2f} ms per step")
+# with the result copies (status + toi) back to pinned host memory after each solve
+st_h = torch.empty(args.queries, dtype=torch.uint8).pin_memory()
+toi_h = torch.empty(args.queries, dtype=torch.float64).pin_memory()
+for variant in ("d2h on the solve stream", "d2h on a third stream"):
+    ds = torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+    e0.record()
+    cs.wait_event(e0)
+    with torch.cuda.stream(cs):
+        for k in range(args.steps):
+            bufs[k % 2].copy_(pts_h, non_blocking=True)
+    for k in range(args.steps):
+        r = solve_batch(pts_d, kind_d, outputs=("status", "toi"), device=dev)
+        if variant.startswith("d2h on the solve"):
+            st_h.copy_(r["status"], non_blocking=True)
+            toi_h.copy_(r["toi"], non_blocking=True)
+        else:
+            ds.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(ds):
+                st_h.copy_(r["status"], non_blocking=True)
+                toi_h.copy_(r["toi"], non_blocking=True)
+    torch.cuda.current_stream().wait_stream(cs)
+    torch.cuda.current_stream().wait_stream(ds)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"copies || solves + {variant}: {e0.elapsed_time(e1) / args.steps:.2f} ms per step")
+# the API's issue order: copy k on the side stream, then solve k and its
+# result copies on the solve stream, then copy k + 1 ...
+torch.cuda.synchronize()
+e0.record()
+cs.wait_event(e0)
+for k in range(args.steps):
+    with torch.cuda.stream(cs):
+        bufs[k % 2].copy_(pts_h, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(cs)
+    r = solve_batch(bufs[k % 2].view(-1, 8, 3), kind_d, outputs=("status", "toi"), device=dev)
+    st_h.copy_(r["status"], non_blocking=True)
+    toi_h.copy_(r["toi"], non_blocking=True)
+e1.record()
+torch.cuda.synchronize()
+print(f"interleaved issue (copy k+1 after result copies k): {e0.elapsed_time(e1) / args.steps:.2f} ms per step")
