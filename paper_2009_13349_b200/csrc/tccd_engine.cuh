@@ -1,20 +1,24 @@
-// Level engine: an independent group of threads (a warp, or a whole CTA)
-// keeps up to Q queries resident and advances all of them one BFS level per
-// round.  One template, three tiers (see tccd.cu): light and medium (one warp
-// per group, many independent groups per SM, warp-synchronous: the latency
-// of one group's memory phases is hidden by the others) and giant (a CTA per
-// query for levels of up to 2 * m_I boxes).  A query whose level outgrows
-// its tier is restarted in the next tier (classification is a pure function
-// of the box, so the replay is exact).
+// Level engine: an independent group of threads (a CTA) keeps up to Q
+// queries resident and advances all of them one BFS level per round.  One
+// template, three tiers (see tccd.cu): light (128-thread CTAs, 5 per SM, 32
+// queries, levels up to 1024 boxes) and medium (256-thread CTAs, 2 per SM,
+// 8 queries, levels up to 8192 boxes), both with their per-box bookkeeping
+// in shared memory, and giant (a 512-thread CTA per query for levels of up
+// to 2 * m_I boxes, bookkeeping in global memory).  A query whose level
+// outgrows its tier moves to the next tier with that level handed over (or,
+// if the handover pool is full, restarts there: classification is a pure
+// function of the box, so the replay is exact).
 //
 // Representation.  The current levels of all resident queries form one flat
 // list of 4-byte references, one segment per query, each segment in the
 // reference's visiting order (stable by t_lo, _kernel.py:174-175).  A
 // reference names a box of the PREVIOUS round's materialized box array:
-// "child cb of box src" (the split is recomputed from the parent, a pure
-// function of the parent box and kappa), "box src itself" (a deferred
-// level), or the query's root.  Children never travel through memory as
-// boxes: the classify phase materializes each box once, in visiting order.
+// "child cb of box src" (the child is the parent with one bound replaced by
+// the midpoint of the parent's split dimension, which the parent's flag
+// byte records), "box src itself" (a deferred level), a box of the tier's
+// handover pool, or the query's root.  Children never travel through memory
+// as boxes: the classify phase materializes each box once, in visiting
+// order.
 //
 // A round:
 //   P1 materialize + classify every box (lane per box, queries mixed);
