@@ -57,9 +57,9 @@ class Query:
         float coordinates read back from a validated batch): the same object,
         without re-validating 24 coordinates one by one."""
         q = object.__new__(cls)
-        object.__setattr__(q, "kind", kind)
-        object.__setattr__(q, "points0", points0)
-        object.__setattr__(q, "points1", points1)
+        q.__dict__["kind"] = kind
+        q.__dict__["points0"] = points0
+        q.__dict__["points1"] = points1
         return q
 
     def as_arrays(self) -> tuple[np.ndarray, np.ndarray]:
@@ -91,10 +91,10 @@ class DomainBox:
     def _trusted(cls, t: tuple, u: tuple, v: tuple, level: int) -> "DomainBox":
         """A DomainBox from a solver witness (nested in [0, 1] by construction)."""
         b = object.__new__(cls)
-        object.__setattr__(b, "t", t)
-        object.__setattr__(b, "u", u)
-        object.__setattr__(b, "v", v)
-        object.__setattr__(b, "level", level)
+        b.__dict__["t"] = t
+        b.__dict__["u"] = u
+        b.__dict__["v"] = v
+        b.__dict__["level"] = level
         return b
 
     @property

@@ -36,7 +36,8 @@ import torch
 
 from . import _lib
 from .core import DomainBox, Query, QueryKind, SolverConfig
-from .inclusion import compute_filters, compute_gamma
+from .inclusion import (EE_COEFF, EE_COEFF_MINSEP, VF_COEFF, VF_COEFF_MINSEP,
+                        compute_filters, compute_gamma)
 from .solver import solve_batch
 
 __all__ = [
@@ -115,6 +116,14 @@ class ContactCandidate:
     indices: tuple
     query: Query
 
+    @classmethod
+    def _trusted(cls, kind, indices, query) -> "ContactCandidate":
+        c = object.__new__(cls)
+        c.__dict__["kind"] = kind
+        c.__dict__["indices"] = indices
+        c.__dict__["query"] = query
+        return c
+
 
 @dataclass
 class CandidateSet:
@@ -145,18 +154,16 @@ class CandidateSet:
         coordinates come from a validated mesh, so the Query objects are
         built without re-checking them)."""
         h = self.host()
-        pts = h.points.tolist()
-        kinds = h.kind.tolist()
-        idx = h.indices.tolist()
         K = (QueryKind.VERTEX_FACE, QueryKind.EDGE_EDGE)
         out = []
+        qt, ct = Query._trusted, ContactCandidate._trusted
         with _bulk():
-            for i in range(h.m):
-                p = pts[i]
-                k = K[kinds[i]]
-                q = Query._trusted(k, (tuple(p[0]), tuple(p[1]), tuple(p[2]), tuple(p[3])),
-                                   (tuple(p[4]), tuple(p[5]), tuple(p[6]), tuple(p[7])))
-                out.append(ContactCandidate(k, (idx[i][0], idx[i][1]), q))
+            flat = h.points.reshape(h.m, 24).tolist()
+            for f, kk, ij in zip(flat, h.kind.tolist(), h.indices.tolist()):
+                it = iter(f)
+                t = tuple(zip(it, it, it))  # the 8 points as (x, y, z) tuples
+                k = K[kk]
+                out.append(ct(k, tuple(ij), qt(k, t[:4], t[4:])))
         return out
 
 
@@ -390,6 +397,88 @@ def distance_lb(kind: int, points8: np.ndarray) -> float:
     return max(0.0, math.nextafter(d / _SQRT3, 0.0))
 
 
+# The same closed forms over a whole candidate batch: every operation is the
+# scalar code's, elementwise in the same order (numpy float64 ufuncs round
+# each operation like Python floats and never contract a multiply-add), and
+# each branch becomes a select of both outcomes, so the bounds are
+# bit-identical to distance_lb's (tests/test_scene.py checks).
+
+def _vsub(a, b):
+    return (a[0] - b[0], a[1] - b[1], a[2] - b[2])
+
+
+def _vadd(a, b):
+    return (a[0] + b[0], a[1] + b[1], a[2] + b[2])
+
+
+def _vscl(a, s):
+    return (a[0] * s, a[1] * s, a[2] * s)
+
+
+def _vdot(a, b):
+    return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]
+
+
+def _vcross(a, b):
+    return (a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0])
+
+
+def _vnorm(v):
+    return np.sqrt(_vdot(v, v))
+
+
+def _vclamp01(s):
+    return np.where(s < 0.0, 0.0, np.where(s > 1.0, 1.0, s))
+
+
+def _vpt_seg(p, a, b):
+    ab = _vsub(b, a)
+    denom = _vdot(ab, ab)
+    s = _vclamp01(_vdot(_vsub(p, a), ab) / denom)
+    return np.where(denom == 0.0, _vnorm(_vsub(p, a)), _vnorm(_vsub(p, _vadd(a, _vscl(ab, s)))))
+
+
+def _vpt_tri(p, a, b, c):
+    best = np.minimum(np.minimum(_vpt_seg(p, a, b), _vpt_seg(p, b, c)), _vpt_seg(p, c, a))
+    n = _vcross(_vsub(b, a), _vsub(c, a))
+    nn = _vdot(n, n)
+    w0 = _vdot(_vcross(_vsub(c, b), _vsub(p, b)), n)
+    w1 = _vdot(_vcross(_vsub(a, c), _vsub(p, c)), n)
+    w2 = _vdot(_vcross(_vsub(b, a), _vsub(p, a)), n)
+    inside = (nn > 0.0) & (w0 >= 0.0) & (w1 >= 0.0) & (w2 >= 0.0)
+    return np.where(inside, np.minimum(best, np.abs(_vdot(_vsub(p, a), n)) / np.sqrt(nn)), best)
+
+
+def _vseg_seg(p1, q1, p2, q2):
+    d1, d2, r = _vsub(q1, p1), _vsub(q2, p2), _vsub(p1, p2)
+    a, e, f = _vdot(d1, d1), _vdot(d2, d2), _vdot(d2, r)
+    c = _vdot(d1, r)
+    b = _vdot(d1, d2)
+    denom = a * e - b * b
+    # general case (a > 0, e > 0)
+    s_g = np.where(denom > 0.0, _vclamp01((b * f - c * e) / denom), 0.0)
+    t_g = (b * s_g + f) / e
+    s_g, t_g = (np.where(t_g < 0.0, _vclamp01(-c / a), np.where(t_g > 1.0, _vclamp01((b - c) / a), s_g)),
+                np.where(t_g < 0.0, 0.0, np.where(t_g > 1.0, 1.0, t_g)))
+    # a == 0: s = 0, t = clamp(f / e); e == 0 (a > 0): t = 0, s = clamp(-c / a)
+    s = np.where(a == 0.0, 0.0, np.where(e == 0.0, _vclamp01(-c / a), s_g))
+    t = np.where(a == 0.0, _vclamp01(f / e), np.where(e == 0.0, 0.0, t_g))
+    d = _vnorm(_vsub(_vadd(p1, _vscl(d1, s)), _vadd(p2, _vscl(d2, t))))
+    return np.where((a == 0.0) & (e == 0.0), _vnorm(r), d)
+
+
+def distance_lb_batch(kind: np.ndarray, points: np.ndarray) -> np.ndarray:
+    """distance_lb of every candidate: kind [m], points [m, 8, 3] (start
+    positions are points[:, :4])."""
+    kind = np.asarray(kind)
+    P = np.asarray(points, dtype=np.float64)
+    pt = [tuple(P[:, k, j] for j in range(3)) for k in range(4)]
+    with np.errstate(all="ignore"):  # (the unselected branch may divide by 0)
+        d = np.where(kind == 0, _vpt_tri(*pt), _vseg_seg(*pt))
+        lb = np.maximum(0.0, np.nextafter(d / _SQRT3, 0.0))
+    return np.where(d <= 0.0, 0.0, lb)
+
+
 def primitive_distance_lb(candidate: ContactCandidate) -> float:
     return distance_lb(int(candidate.kind), candidate.query.all_coordinates())
 
@@ -405,6 +494,16 @@ class CandidateBound:
     separation: float
     toi: float | None
     witness: DomainBox | None
+
+    @classmethod
+    def _trusted(cls, candidate, distance_lb, separation, toi, witness) -> "CandidateBound":
+        b = object.__new__(cls)
+        b.__dict__["candidate"] = candidate
+        b.__dict__["distance_lb"] = distance_lb
+        b.__dict__["separation"] = separation
+        b.__dict__["toi"] = toi
+        b.__dict__["witness"] = witness
+        return b
 
 
 @dataclass(frozen=True)
@@ -433,22 +532,30 @@ def line_search_step(mesh: TriMeshPair, *, p: float, delta: float = 1e-6,
     cs = broad_phase_batch(mesh, inflation, device=device)
     hc = cs.host()
     m = cs.m
-    d_lb = np.empty(m)
-    eps_max = np.empty(m)
-    for i in range(m):
-        d_lb[i] = distance_lb(int(hc.kind[i]), hc.points[i])
-        if d_lb[i] <= 0.0:
+    # start-distance bounds and the filters of every candidate, batched; the
+    # first failing candidate raises what the reference's loop raises first
+    d_lb = distance_lb_batch(hc.kind, hc.points)
+    sep0 = np.minimum(p * d_lb, delta)
+    gam = np.maximum(1.0, np.abs(hc.points).max(axis=1))  # compute_gamma per candidate
+    bad_sep = (sep0 > 0.0) & ~np.all(sep0[:, None] < gam, axis=1)
+    bad_d = d_lb <= 0.0
+    first_bad = int(np.argmax(bad_d | bad_sep)) if bool((bad_d | bad_sep).any()) else -1
+    if first_bad >= 0:
+        i = first_bad
+        if bad_d[i]:
             raise InfeasibleStepError(
                 f"{QueryKind(int(hc.kind[i])).name} pair {tuple(int(x) for x in hc.indices[i])} "
                 "touches at the step start; no positive step can be certified")
-        fe = compute_filters(QueryKind(int(hc.kind[i])), compute_gamma(hc.points[i]),
-                             separation=min(p * d_lb[i], delta))
-        eps_max[i] = max(fe.eps)
+        compute_filters(QueryKind(int(hc.kind[i])), tuple(float(g) for g in gam[i]),
+                        separation=float(sep0[i]))  # (raises the reference's ValueError)
+    coeff = np.where(hc.kind == 0, np.where(sep0 > 0.0, VF_COEFF_MINSEP, VF_COEFF),
+                     np.where(sep0 > 0.0, EE_COEFF_MINSEP, EE_COEFF))
+    eps_max = (coeff[:, None] * (gam * gam * gam)).max(axis=1)  # max(compute_filters(...).eps)
 
     def worst_ratio(tol):
-        return min((float(d) - tol - float(e) - _DISTANCE_SLACK) / float(d)
-                   for d, e in zip(d_lb, eps_max))
+        return float(np.min((d_lb - tol - eps_max - _DISTANCE_SLACK) / d_lb)) if m else 0.0
 
+    cands = hc.to_list() if m else []
     alpha, validations, bounds, limiting = 1.0, 0, [], None
     tol_assumed = delta
     while m:
@@ -459,7 +566,7 @@ def line_search_step(mesh: TriMeshPair, *, p: float, delta: float = 1e-6,
             if p == 0.0:
                 raise InfeasibleStepError("validation halved p to zero; the start distances "
                                           "cannot cover the solver tolerance plus numeric error")
-        seps = [min(p * float(d), delta) for d in d_lb]
+        seps = np.minimum(p * d_lb, delta)
         alpha, achieved, limiting = 1.0, tol_assumed, None
         bounds = []
         i0 = 0
@@ -468,20 +575,36 @@ def line_search_step(mesh: TriMeshPair, *, p: float, delta: float = 1e-6,
             # the first one that lowers alpha
             cfg = SolverConfig(delta=tol_assumed, max_checks=max_checks, t_max=alpha)
             r = _solve(cs, slice(i0, m), cfg, seps[i0:], device)
+            hit = r["status"] == 1
+            toi = r["toi"]
+            lower = hit & (toi < alpha)
+            lowered = bool(lower.any())
+            j_end = int(np.argmax(lower)) + 1 if lowered else m - i0
+            # a free result carries codomain width 0 (solver.py:89-93)
+            if j_end:
+                achieved = max(achieved, float(np.max(np.where(hit[:j_end], r["codom"][:j_end], 0.0))))
+            toi_l = toi[:j_end].tolist()
+            hit_l = hit[:j_end].tolist()
+            w = r["witness"][:j_end].tolist()
+            lv = r["level"][:j_end].tolist()
+            d_l = d_lb[i0:i0 + j_end].tolist()
+            s_l = seps[i0:i0 + j_end].tolist()
+            with _bulk():
+                for j in range(j_end):
+                    if hit_l[j]:
+                        wj = w[j]
+                        bounds.append(CandidateBound._trusted(
+                            cands[i0 + j], d_l[j], s_l[j], toi_l[j],
+                            DomainBox._trusted((wj[0], wj[1]), (wj[2], wj[3]), (wj[4], wj[5]),
+                                               lv[j])))
+                    else:
+                        bounds.append(CandidateBound._trusted(cands[i0 + j], d_l[j], s_l[j],
+                                                              None, None))
             nxt = m
-            for k in range(i0, m):
-                j = k - i0
-                hit = r["status"][j] == 1
-                toi = float(r["toi"][j]) if hit else None
-                # a free result carries codomain width 0 (solver.py:89-93)
-                achieved = max(achieved, float(r["codom"][j]) if hit else 0.0)
-                bounds.append(CandidateBound(hc.candidate(k), float(d_lb[k]), seps[k], toi,
-                                             _witness(r, j) if hit else None))
-                if hit and toi < alpha:
-                    alpha = toi
-                    limiting = len(bounds) - 1
-                    nxt = k + 1
-                    break
+            if lowered:
+                alpha = toi_l[j_end - 1]
+                limiting = len(bounds) - 1
+                nxt = i0 + j_end
             if alpha == 0.0:
                 break  # the remaining interval is empty
             i0 = nxt

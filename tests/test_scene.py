@@ -308,3 +308,28 @@ def test_line_search_gpu_matches_sequential_oracle_large():
                     break
     assert r.validations == 1 and _bits(r.alpha) == _bits(alpha) and r.limiting == lim
     assert math.isfinite(r.alpha)
+
+
+@pytest.mark.parametrize("family", ["uniform", "lattice", "degenerate", "coplanar"])
+def test_distance_lb_batch_matches_scalar(family):
+    """The batched start-distance bounds (line_search_step's) equal the scalar
+    closed forms bit for bit, branches included (zero-length edges, parallel
+    edges, degenerate triangles)."""
+    from paper_2009_13349_b200.scene import distance_lb, distance_lb_batch
+    rng = np.random.default_rng(3)
+    m = 4000
+    if family == "uniform":
+        pts = rng.random((m, 8, 3))
+    elif family == "lattice":
+        pts = rng.integers(-3, 4, (m, 8, 3)) / 2.0
+    elif family == "degenerate":
+        pts = rng.random((m, 8, 3))
+        pts[:, 1] = pts[:, 0]
+        pts[::3, 3] = pts[::3, 2]
+    else:
+        pts = rng.random((m, 8, 3))
+        pts[..., 2] = 0.0
+    kind = rng.integers(0, 2, m).astype(np.uint8)
+    got = distance_lb_batch(kind, pts)
+    want = np.array([distance_lb(int(kind[i]), pts[i]) for i in range(m)])
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))

@@ -24,7 +24,8 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2009_13349_b200.scene import (TriMeshPair, active_set_batch,  # noqa: E402
-                                         broad_phase_batch, construct_active_set)
+                                         broad_phase_batch, construct_active_set,
+                                         line_search_step)
 
 
 def cloth(g: int, seed: int = 0) -> TriMeshPair:
@@ -75,6 +76,12 @@ def main():
             "active_set_batch_ms": act_ms, "active_pairs": hits.m,
             "construct_active_set_list_ms": list_ms}
     assert len(act) == hits.m
+    # line_search_step (scene.py:468-583): broad phase, start-distance bounds
+    # and filters of every candidate, solves at the shrinking alpha
+    t0 = time.perf_counter()
+    ls = line_search_step(mesh, p=0.5)
+    line.update({"line_search_ms": 1e3 * (time.perf_counter() - t0), "line_search_alpha": ls.alpha,
+                 "line_search_validations": ls.validations, "line_search_bounds": len(ls.bounds)})
     if not args.no_host:
         # bounded host sample: the numpy restatement on a 60 x 60 cloth
         from scene_host import broad_phase_host
