@@ -337,6 +337,11 @@ struct EngineShared {
   unsigned long long sw[2 * (Cfg::G / 32)];
   int swi[4 * (Cfg::G / 32)];
   int any_general;
+  // one-query tier, dyadic t_max: every box of a level has the same widths,
+  // so a materialized box is stored as its lower corner (t0, u0, v0) only
+  double w[3];           // widths of the current level's boxes
+  double wp[3];          // widths of the previous level's (the parents')
+  int lvl_sdim;          // split dimension of the current level's refining boxes
   int n_cur, n_next, admit_k, exhausted, A_tot, B_tot, P_tot, rot;
   unsigned long long deferred;
   int deferred_last;     // queries deferred in the previous round
@@ -599,10 +604,17 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       S.uniform[s] = frexp(S.qp[s].t_max, &ex) == 0.5;  // t_max a power of two
       int nr = 1;
       long long off = -1;
+      if constexpr (ONEQ) {  // (root widths; a handed-over level's below)
+        S.w[0] = S.qp[s].t_max; S.w[1] = 1.0; S.w[2] = 1.0;
+      }
       if (io.in_hand && io.in_hand[entry(S.admit_base + r)].n > 0) {
         const Hand& hd = io.in_hand[entry(S.admit_base + r)];
         nr = hd.n;
         off = hd.off;
+        if constexpr (ONEQ) {
+          const Box pb = io.in_pbox[off];
+          S.w[0] = pb.t1 - pb.t0; S.w[1] = pb.u1 - pb.u0; S.w[2] = pb.v1 - pb.v0;
+        }
         S.C[s] = hd.C;
         S.level[s] = hd.level;
         S.rec[s][0] = hd.rec[0];
@@ -683,17 +695,38 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     const int n1 = ONEQ ? (int)min((long long)n, S.seg_off[0] + max(S.qp[0].max_checks - S.C[0], 0ll))
                         : n;
     boxes += (unsigned long long)n1;
+    // compact boxes (one query, dyadic t_max): the level arrays hold lower
+    // corners; a parent (of the previous level) is completed with wp
+    const bool compact = ONEQ && S.uniform[0];
+    const double* const cprev = reinterpret_cast<const double*>(bprev);
+    double* const ccur = reinterpret_cast<double*>(bx);
+    // load box r of the previous level or of the pool into o (a compact
+    // parent only with its lower corner: completed when it is used)
+    auto fetch = [&](unsigned int r, Box& o) {
+      if (!(r & kRefRoot)) {
+        if (compact) {
+          const double* q = cprev + 3 * (size_t)(r & kRefSrcMask);
+          o.t0 = q[0]; o.u0 = q[1]; o.v0 = q[2];
+        } else {
+          o = bprev[r & kRefSrcMask];
+        }
+      } else if ((r & kRefExt) == kRefExt) {
+        o = pool[r & kRefSrcMask];
+      }
+    };
+    // a box of the current level (compact: completed with the level's widths)
+    auto box_at = [&](int x) -> Box {
+      if (!compact) return bx[x];
+      const double* q = ccur + 3 * (size_t)x;
+      return Box{q[0], q[0] + S.w[0], q[1], q[1] + S.w[1], q[2], q[2] + S.w[2]};
+    };
     unsigned int r_cur = tid < n1 ? rf[tid] : kRefRoot;
     Box p_cur;
     // (global tier: the parent's flag byte travels with the parent box)
     const uint8_t* const flp = pick(flags, prv);
     uint8_t pf_cur = 0;
-    if (!(r_cur & kRefRoot)) {
-      p_cur = bprev[r_cur & kRefSrcMask];
-      if constexpr (!Cfg::SMEM) pf_cur = flp[r_cur & kRefSrcMask];
-    } else if ((r_cur & kRefExt) == kRefExt) {
-      p_cur = pool[r_cur & kRefSrcMask];
-    }
+    fetch(r_cur, p_cur);
+    if (!Cfg::SMEM && !(r_cur & kRefRoot)) pf_cur = flp[r_cur & kRefSrcMask];
     unsigned int r_nxt = tid + NT < n1 ? rf[tid + NT] : kRefRoot;
     // (global flags: prefetched one iteration ahead as well)
     uint8_t f_cur = 0;
@@ -707,15 +740,15 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       }
       Box p_nxt;
       uint8_t pf_nxt = 0;
-      if (!(r_nxt & kRefRoot)) {
-        p_nxt = bprev[r_nxt & kRefSrcMask];
-        if constexpr (!Cfg::SMEM) pf_nxt = flp[r_nxt & kRefSrcMask];
-      } else if ((r_nxt & kRefExt) == kRefExt) {
-        p_nxt = pool[r_nxt & kRefSrcMask];
-      }
+      fetch(r_nxt, p_nxt);
+      if (!Cfg::SMEM && !(r_nxt & kRefRoot)) pf_nxt = flp[r_nxt & kRefSrcMask];
       const unsigned int r_nn = i + 2 * NT < n1 ? rf[i + 2 * NT] : kRefRoot;
       const unsigned int r = r_cur;
-      const Box p = p_cur;
+      Box p = p_cur;
+      if (compact && !(r & kRefRoot)) {  // complete the parent (or the box itself)
+        const double* wq = (r & kRefSelf) ? S.w : S.wp;
+        p.t1 = p.t0 + wq[0]; p.u1 = p.u0 + wq[1]; p.v1 = p.v0 + wq[2];
+      }
       const uint8_t pf = pf_cur;
       pf_cur = pf_nxt;
       r_cur = r_nxt;
@@ -778,7 +811,15 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         // only non-disjoint boxes are read again (parents, first / drop
         // records, merge keys): disjoint ones are never stored, which keeps
         // the level arrays' footprint in L2
-        bx[i] = b;
+        if (compact) {
+          double* q = ccur + 3 * (size_t)i;
+          q[0] = b.t0; q[1] = b.u0; q[2] = b.v0;
+          // (classified here or carried, e.g. the root's: the same for every
+          // refining box of the level)
+          if (!(f & 4)) S.lvl_sdim = (f >> 3) & 3;
+        } else {
+          bx[i] = b;
+        }
         wbc[i] = wb;
         atomicMin(&S.j[s], k);
         // first accepted box: if it is not j itself it lies after j, and it is
@@ -827,7 +868,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         }
       } else {
         const int ij = S.seg_off[s] + j;
-        const Box bj = bx[ij];
+        const Box bj = box_at(ij);
         const double wbj = wbc[ij];
         Rec& fr = S.rec[s][0];
         fr.b = bj;
@@ -848,7 +889,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           const long long eend = nn < cut ? nn : cut;
           const int ai = S.acc[s];
           if (ai < eend) {
-            const Box ba = bx[S.seg_off[s] + ai];
+            const Box ba = box_at(S.seg_off[s] + ai);
             if (!S.have_drop[s] || ba.t0 < S.rec[s][1].b.t0) {
               Rec& dr = S.rec[s][1];
               dr.b = ba;
@@ -1329,6 +1370,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         S.seg_n[s] = S.tot[s];
         S.level[s] += 1;
         S.seg_off[s] = S.next_off[s];
+        if (compact) {  // the next level's boxes: this level's split dimension halved
+          S.wp[0] = S.w[0]; S.wp[1] = S.w[1]; S.wp[2] = S.w[2];
+          S.w[S.lvl_sdim] = 0.5 * S.w[S.lvl_sdim];
+        }
       } else if (S.cont[s] == 2) {
         S.C[s] -= S.seg_n[s];  // the level re-runs next round
         S.seg_off[s] = S.next_off[s];
