@@ -12,7 +12,7 @@
 //  2. engine_kernel tiers (tccd_engine.cuh), each a persistent grid whose
 //     independent groups keep several queries resident and advance them one
 //     BFS level per round with lane-per-box classification:
-//        light  : 128-thread CTA (5 per SM), 32 queries, levels <= 1024
+//        light  : 128-thread CTA (5 per SM), 40 queries, levels <= 1024
 //                 boxes, per-box bookkeeping in shared memory
 //        medium : 256-thread CTA (2 per SM), 8 queries, levels <= 8192
 //                 boxes, per-box bookkeeping in shared memory
@@ -260,10 +260,10 @@ namespace tccd {
 
 //                   G    NT   Q   CAP    QCAP   ADMIT  SMEM   MINB
 #ifndef TCCD_LQ
-#define TCCD_LQ 32
+#define TCCD_LQ 40
 #endif
 #ifndef TCCD_LADMIT
-#define TCCD_LADMIT 1024
+#define TCCD_LADMIT 1280
 #endif
 #ifndef TCCD_LQCAP
 #define TCCD_LQCAP 1024
@@ -275,7 +275,7 @@ namespace tccd {
 #define TCCD_LNT 128
 #endif
 #ifndef TCCD_LCAP
-#define TCCD_LCAP 3072
+#define TCCD_LCAP 3840
 #endif
 #ifndef TCCD_LMINB
 #define TCCD_LMINB 5

@@ -1,6 +1,6 @@
 // Level engine: an independent group of threads (a CTA) keeps up to Q
 // queries resident and advances all of them one BFS level per round.  One
-// template, three tiers (see tccd.cu): light (128-thread CTAs, 5 per SM, 32
+// template, three tiers (see tccd.cu): light (128-thread CTAs, 5 per SM, 40
 // queries, levels up to 1024 boxes) and medium (256-thread CTAs, 2 per SM,
 // 8 queries, levels up to 8192 boxes), both with their per-box bookkeeping
 // in shared memory, and giant (a 512-thread CTA per query for levels of up
