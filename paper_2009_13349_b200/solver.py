@@ -132,6 +132,9 @@ def _param(x, n, dtype, device, name):
     return t.to(device=device, dtype=dtype, non_blocking=True).contiguous(), 0
 
 
+CHUNK = 1 << 22  # queries per library chunk (csrc/tccd.cu kChunk)
+
+
 def _params(kind, config, delta, max_checks, separation, t_max, n, dev):
     """Per-query (device tensor) or broadcast (scalar) kind, delta,
     max_checks, separation and t_max; unset ones from ``config``."""
@@ -202,19 +205,32 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
     if host_in:
         pts = pts.contiguous().pin_memory() if pts.device.type == "cpu" else pts
     slot = None
+    chunk_events = None  # (a batch above one library chunk: per-chunk copy events)
     if host_in and non_blocking:
         # every host input goes over on the API's copy stream: an engine copy
         # issued on the launching stream would queue behind the solve already
-        # there and hold back the next call's copies
+        # there and hold back the next call's copies.  A batch of several
+        # library chunks is copied chunk by chunk, each chunk's solve waiting
+        # only for its own points, so the copy overlaps the solve inside one
+        # call as well.
         compute = torch.cuda.current_stream(dev)
         cs = copy_stream(dev)
         slot = _staging_buffer(dev, pts.numel() * 8)
         with torch.cuda.stream(cs):
             dst = slot[0][:pts.numel() * 8].view(torch.float64).view(pts.shape)
-            dst.copy_(pts, non_blocking=True)
             kind_t, kind_all, delta_t, delta_all, mc_t, mc_all, sep_t, sep_all, tm_t, tm_all, \
                 mc_src, sep_src = _params(kind, config, delta, max_checks, separation, t_max, n, dev)
-        compute.wait_stream(cs)
+            if n > CHUNK and stats is False and events is None:
+                chunk_events = []
+                for lo in range(0, n, CHUNK):
+                    dst[lo:lo + CHUNK].copy_(pts[lo:lo + CHUNK], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                    chunk_events.append(ev)
+            else:
+                dst.copy_(pts, non_blocking=True)
+        if chunk_events is None:
+            compute.wait_stream(cs)
         for t in (dst, kind_t, delta_t, mc_t, sep_t, tm_t):
             if t is not None:
                 t.record_stream(compute)  # (allocated on the copy stream, read by the solve)
@@ -270,34 +286,46 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
         hb = heavy_blocks or default_heavy_blocks(dev, n, mc_max)
         nbytes = workspace_bytes(n, mc_max, hb)
         ws = _workspace(dev, nbytes)
-        b = _lib.TccdBatch()
-        b.struct_size = ctypes.sizeof(_lib.TccdBatch)
-        b.flags = _lib.FLAG_HEAVY_ONLY if heavy_only else 0
-        b.n = n
-        b.points = _ptr(pts)
-        b.kind = _ptr(kind_t)
-        b.kind_all = kind_all
-        b.delta = _ptr(delta_t)
-        b.delta_all = float(delta_all)
-        b.max_checks = _ptr(mc_t)
-        b.max_checks_all = int(mc_all)
-        b.max_checks_max = mc_max
-        b.separation = _ptr(sep_t)
-        b.separation_all = float(sep_all)
-        b.t_max = _ptr(tm_t)
-        b.t_max_all = float(tm_all)
-        b.eps = _ptr(eps_t)
-        for k in OUTPUT_FIELDS:
-            setattr(b, k, _ptr(out.get(k)))
-        b.workspace = _ptr(ws)
-        b.workspace_bytes = ws.numel()
-        b.heavy_blocks = hb
-        b.device_sms = sm_count(dev)
-        b.stats = _ptr(st)
-        b.events = ctypes.cast(ev_arr, ctypes.c_void_p) if ev_arr is not None else None
         stream = torch.cuda.current_stream(dev)
-        rc = lib.tccd_solve_batch(ctypes.byref(b), ctypes.c_void_p(stream.cuda_stream))
-        _raise_abi(rc, delta_all, mc_all, tm_all, sep_all, kind_all)
+
+        def sl(t, lo, hi):
+            return None if t is None else t[lo:hi]
+
+        def launch(lo, hi, ev_arr=None):
+            b = _lib.TccdBatch()
+            b.struct_size = ctypes.sizeof(_lib.TccdBatch)
+            b.flags = _lib.FLAG_HEAVY_ONLY if heavy_only else 0
+            b.n = hi - lo
+            b.points = _ptr(pts[lo:hi])
+            b.kind = _ptr(sl(kind_t, lo, hi))
+            b.kind_all = kind_all
+            b.delta = _ptr(sl(delta_t, lo, hi))
+            b.delta_all = float(delta_all)
+            b.max_checks = _ptr(sl(mc_t, lo, hi))
+            b.max_checks_all = int(mc_all)
+            b.max_checks_max = mc_max
+            b.separation = _ptr(sl(sep_t, lo, hi))
+            b.separation_all = float(sep_all)
+            b.t_max = _ptr(sl(tm_t, lo, hi))
+            b.t_max_all = float(tm_all)
+            b.eps = _ptr(sl(eps_t, lo, hi))
+            for k in OUTPUT_FIELDS:
+                setattr(b, k, _ptr(sl(out.get(k), lo, hi)))
+            b.workspace = _ptr(ws)
+            b.workspace_bytes = ws.numel()
+            b.heavy_blocks = hb
+            b.device_sms = sm_count(dev)
+            b.stats = _ptr(st)
+            b.events = ctypes.cast(ev_arr, ctypes.c_void_p) if ev_arr is not None else None
+            rc = lib.tccd_solve_batch(ctypes.byref(b), ctypes.c_void_p(stream.cuda_stream))
+            _raise_abi(rc, delta_all, mc_all, tm_all, sep_all, kind_all)
+
+        if chunk_events is None:
+            launch(0, n, ev_arr)
+        else:
+            for c, ev in enumerate(chunk_events):
+                stream.wait_event(ev)
+                launch(c * CHUNK, min(n, (c + 1) * CHUNK))
     if host_in and non_blocking:
         # results into pinned host tensors by a copy kernel on the launching
         # stream, not the copy engines: engine copies are served in submission

@@ -350,3 +350,10 @@ def test_multi_chunk_batch(cuda):
     tail = slice(n - 2_000, n)
     ref = oracle.solve_batch(w.points[tail], w.kind[tail], w.delta, w.max_checks)
     assert_same_results({k: v[tail].cpu().numpy() for k, v in big.items()}, ref, "last chunk")
+    # the streaming host path copies and solves chunk by chunk: same results
+    hp = torch.from_numpy(w.points).pin_memory()
+    hk = torch.from_numpy(w.kind).pin_memory()
+    st = solve_batch(hp, hk, device=cuda, non_blocking=True)
+    st["ready"].synchronize()
+    for k in ("status", "toi", "checks", "witness", "level"):
+        assert torch.equal(st[k], big[k].cpu()), k
