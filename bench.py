@@ -374,7 +374,10 @@ def main():
                      "ncu_counters": ncu_counters},
         "cpu_baseline": cpu,
         "clocks": clk,
-        "gpu_launches": 2 * args.steps * LAUNCHES_PER_SOLVE * ((Q + (1 << 22) - 1) >> 22),
+        # timed device steps + timed e2e steps (whose two result copy-outs,
+        # status and toi, are kernels too)
+        "gpu_launches": args.steps * LAUNCHES_PER_SOLVE * nch
+                        + args.steps * (LAUNCHES_PER_SOLVE * nch + 2),
         "workload_stats": {"hits": hits, "hit_rate": hits / Q, "mean_checks": float(checks.mean()),
                            "max_checks": int(checks.max()), "giant_tier_queries": evicted,
                            "engine_rounds": pool_rounds, "level_deferrals": deferrals,
