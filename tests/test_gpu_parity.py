@@ -357,3 +357,23 @@ def test_multi_chunk_batch(cuda):
     st["ready"].synchronize()
     for k in ("status", "toi", "checks", "witness", "level"):
         assert torch.equal(st[k], big[k].cpu()), k
+
+
+def test_non_blocking_edge_cases(cuda):
+    """The streaming host path with an empty batch, and with per-query host
+    parameters (copied on the API's side stream too)."""
+    from paper_2009_13349_b200 import solve_batch
+    from paper_2009_13349_b200 import workloads as W
+    e = solve_batch(torch.zeros((0, 8, 3), dtype=torch.float64).pin_memory(),
+                    torch.zeros(0, dtype=torch.uint8).pin_memory(), device=cuda, non_blocking=True)
+    e["ready"].synchronize()
+    assert e["status"].numel() == 0 and e["toi"].numel() == 0
+    w = W.generate(2, 0, 3000)
+    mc = np.minimum(w.max_checks, 20_000)
+    got = solve_batch(torch.from_numpy(w.points).pin_memory(), torch.from_numpy(w.kind).pin_memory(),
+                      delta=torch.from_numpy(w.delta), max_checks=torch.from_numpy(mc),
+                      device=cuda, non_blocking=True)
+    got["ready"].synchronize()
+    ref = oracle.solve_batch(w.points, w.kind, w.delta, mc)
+    assert_same_results({k: v.numpy() for k, v in got.items() if k not in ("ready",)}, ref,
+                        "non-blocking per-query")
