@@ -29,6 +29,7 @@
 // Pass 3: pass 1's thread-per-query search with max_checks + 2 heap entries.
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 #include <cstring>
 
@@ -202,7 +203,10 @@ struct Heap {
 };
 
 // One query; returns false if the heap outgrew its capacity (re-run later).
-__device__ bool irf_query(const Args& a, long long q, Heap& H) {
+// check_cap: pass 1 gives up on a query after this many checks (a long
+// best-first search is far faster as a warp's run search, pass 2); the
+// fallback pass 3 runs without it
+__device__ bool irf_query(const Args& a, long long q, Heap& H, long long check_cap) {
   double P[24];
   bool finite = true;
 #pragma unroll
@@ -249,6 +253,7 @@ __device__ bool irf_query(const Args& a, long long q, Heap& H) {
         break;
       }
       ++checks;
+      if (checks > check_cap) return false;  // (re-run from the root by pass 2)
       if (!all) {
         H.pop_discard();
         continue;
@@ -352,6 +357,57 @@ struct RunHeap {             // 8-ary min-heap on (tl, ls); lane 0 only
 };
 
 constexpr int kWarps2 = 4;  // warps per block in pass 2
+constexpr int kFront = 8;   // runs kept in shared memory in front of the run heap
+
+// The run heap with a small front buffer in shared memory (lane 0 only).  A
+// best-first dive pushes one or two runs per step and pops one of them next:
+// those stay in the buffer, and the global heap (a chain of dependent loads
+// per operation) is touched only when the buffer overflows (its largest run
+// moves to the heap) or the heap's top (cached) is smaller than every
+// buffered run.  Keys are unique, so the pop order is the heap's.
+struct FrontRuns {
+  REnt* buf;
+  int nb;
+  RunHeap* H;
+  Key top;  // H->e[0]'s key while H->n > 0
+  __device__ long long size() const { return nb + H->n; }
+  __device__ void refresh() {
+    if (H->n) top = Key{H->e[0].tl, H->e[0].ls};
+  }
+  __device__ void push(const REnt& x) {
+    if (nb < kFront) { buf[nb++] = x; return; }
+    int mi = -1;  // the largest of the buffer and x goes to the heap
+    Key mk{x.tl, x.ls};
+    for (int j = 0; j < kFront; ++j) {
+      const Key kj{buf[j].tl, buf[j].ls};
+      if (key_less(mk, kj)) { mk = kj; mi = j; }
+    }
+    if (mi < 0) {
+      H->push(x);
+    } else {
+      const REnt y = buf[mi];
+      buf[mi] = x;
+      H->push(y);
+    }
+    refresh();
+  }
+  __device__ REnt pop() {  // size() > 0
+    int bi = -1;
+    Key bk{0.0, 0ull};
+    for (int j = 0; j < nb; ++j) {
+      const Key kj{buf[j].tl, buf[j].ls};
+      if (bi < 0 || key_less(kj, bk)) { bk = kj; bi = j; }
+    }
+    if (bi >= 0 && (H->n == 0 || key_less(bk, top))) {
+      const REnt r = buf[bi];
+      buf[bi] = buf[--nb];
+      return r;
+    }
+    const REnt r = H->pop();
+    refresh();
+    return r;
+  }
+};
 
 __device__ __forceinline__ void write_irf_result(const Args& a, long long q, uint8_t st,
                                                  const double b[6], double cw, long long checks,
@@ -369,7 +425,7 @@ __device__ __forceinline__ void write_irf_result(const Args& a, long long q, uin
 
 // One query by one warp; returns false if its run heap filled up (pass 3).
 __device__ bool irf_warp_query(const Args& a, long long q, double2* box, long long bcap,
-                               RunHeap& H, double* Psm) {
+                               RunHeap& H, double* Psm, REnt* front) {
   const int lane = threadIdx.x & 31;
   bool finite = true;
   if (lane < 24) {
@@ -401,11 +457,15 @@ __device__ bool irf_warp_query(const Args& a, long long q, double2* box, long lo
     box[3 * i + 1] = make_double2(b[2], b[3]);
     box[3 * i + 2] = make_double2(b[4], b[5]);
   };
+  FrontRuns F;  // (lane 0's)
+  F.buf = front;
+  F.nb = 0;
+  F.H = &H;
   if (lane == 0) {
     const double root[6] = {0.0, t_max, 0.0, 1.0, 0.0, 1.0};
     stbox(0, root);
     H.n = 0;
-    H.push(REnt{0.0, 0ull, 0, 1, 0});
+    F.push(REnt{0.0, 0ull, 0, 1, 0});
   }
   long long lo_top = 1, hi_top = bcap - 1;  // next free box upward / downward
   unsigned long long cseq = 1;              // run creation order
@@ -414,8 +474,8 @@ __device__ bool irf_warp_query(const Args& a, long long q, double2* box, long lo
     REnt r;
     int empty = 0;
     if (lane == 0) {
-      if (H.n == 0) empty = 1;
-      else r = H.pop();
+      if (F.size() == 0) empty = 1;
+      else r = F.pop();
     }
     if (__shfl_sync(0xffffffffu, empty, 0)) {
       if (lane == 0) write_irf_result(a, q, 0, zero6, 0.0, C, 0, 0);
@@ -512,7 +572,7 @@ __device__ bool irf_warp_query(const Args& a, long long q, double2* box, long lo
           if (up_open && up_cnt > 0) {
             if (lane == 0) {
               if (H.n >= H.cap) full = true;
-              else H.push(REnt{up_key, lv1 | cseq, (int)up_start, -(int)up_cnt, 0});
+              else F.push(REnt{up_key, lv1 | cseq, (int)up_start, -(int)up_cnt, 0});
             }
             ++cseq;
             hi_top = up_start - up_cnt;
@@ -531,11 +591,11 @@ __device__ bool irf_warp_query(const Args& a, long long q, double2* box, long lo
     if (lane == 0) {
       if (main_cnt > 0) {
         if (H.n >= H.cap) full = true;
-        else H.push(REnt{r.tl, lv1 | cseq, (int)main_off, (int)main_cnt, 0});
+        else F.push(REnt{r.tl, lv1 | cseq, (int)main_off, (int)main_cnt, 0});
       }
       if (up_open && up_cnt > 0) {
         if (H.n >= H.cap) full = true;
-        else H.push(REnt{up_key, lv1 | (cseq + 1), (int)up_start, -(int)up_cnt, 0});
+        else F.push(REnt{up_key, lv1 | (cseq + 1), (int)up_start, -(int)up_cnt, 0});
       }
     }
     cseq += 2;
@@ -551,6 +611,7 @@ __global__ void __launch_bounds__(32 * kWarps2) irf_warp_kernel(Args a, Ctr* ctr
                                                                 const long long* list,
                                                                 long long* fallback) {
   __shared__ double Psm[kWarps2][24];
+  __shared__ REnt front[kWarps2][kFront];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long slot = (long long)blockIdx.x * kWarps2 + w;
   unsigned char* mine = arena + slot * (bcap * 48 + hcap * (long long)sizeof(REnt));
@@ -566,16 +627,18 @@ __global__ void __launch_bounds__(32 * kWarps2) irf_warp_kernel(Args a, Ctr* ctr
     i = __shfl_sync(0xffffffffu, i, 0);
     if (i >= total) break;
     const long long q = list[i];
-    if (!irf_warp_query(a, q, box, bcap, H, Psm[w]) && lane == 0)
+    if (!irf_warp_query(a, q, box, bcap, H, Psm[w], front[w]) && lane == 0)
       fallback[atomicAdd(&ctr->fallback, 1ull)] = q;
   }
 }
 
 // pass 0: every query (index list = identity); pass 2: pass 2's fallback list.
 // Per thread: cap keys (16 B) then cap boxes (48 B), contiguous.
+constexpr long long kPass1Checks = 1LL << 14;  // pass 1's check cap (see irf_query)
+
 __global__ void __launch_bounds__(128) irf_kernel(Args a, Ctr* ctr, unsigned char* arena,
                                                   long long cap, const long long* list,
-                                                  long long* overflow, int pass) {
+                                                  long long* overflow, int pass, int has_pass2) {
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   Heap H;
   unsigned char* mine = arena + tid * cap * 64;
@@ -588,7 +651,7 @@ __global__ void __launch_bounds__(128) irf_kernel(Args a, Ctr* ctr, unsigned cha
     const unsigned long long i = atomicAdd(&ctr->next[pass], 1ull);
     if (i >= total) break;
     const long long q = pass == 0 ? (long long)i : list[i];
-    if (!irf_query(a, q, H)) {
+    if (!irf_query(a, q, H, pass == 0 && has_pass2 ? kPass1Checks : LLONG_MAX)) {
       if (pass == 0) overflow[atomicAdd(&ctr->overflow, 1ull)] = q;
       else a.status[q] = 0xFF;  // unreachable: a heap never exceeds checks + 1 <= cap - 1
     }
@@ -728,7 +791,7 @@ int tccd_irf_batch(const tccd_batch* b, void* stream) {
     irf_fill_all<<<(unsigned)((b->n + 255) / 256), 256, 0, st>>>(b->n, ovf, ctr);
   } else {
     irf_kernel<<<(unsigned)(L.threads1 / kThreads), kThreads, 0, st>>>(
-        a, ctr, ws + L.arena1, kCap1, nullptr, ovf, 0);
+        a, ctr, ws + L.arena1, kCap1, nullptr, ovf, 0, L.warps2 > 0 ? 1 : 0);
   }
   if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
   // pass 2 (returns at once when nothing overflowed): warp per query over runs
@@ -742,7 +805,7 @@ int tccd_irf_batch(const tccd_batch* b, void* stream) {
   }
   // pass 3 (a no-op when nothing fell back): max_checks + 2 heap entries per slot
   irf_kernel<<<(unsigned)(L.slots3 / 32), 32, 0, st>>>(a, ctr, ws + L.arena2, L.cap3,
-                                                       L.warps2 > 0 ? fb : ovf, nullptr, 2);
+                                                       L.warps2 > 0 ? fb : ovf, nullptr, 2, 0);
   if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
   return TCCD_OK;
 }
