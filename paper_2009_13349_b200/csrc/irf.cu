@@ -634,7 +634,10 @@ __global__ void __launch_bounds__(32 * kWarps2) irf_warp_kernel(Args a, Ctr* ctr
 
 // pass 0: every query (index list = identity); pass 2: pass 2's fallback list.
 // Per thread: cap keys (16 B) then cap boxes (48 B), contiguous.
-constexpr long long kPass1Checks = 1LL << 14;  // pass 1's check cap (see irf_query)
+#ifndef TCCD_IRF_PASS1_CHECKS
+#define TCCD_IRF_PASS1_CHECKS (1LL << 9)
+#endif
+constexpr long long kPass1Checks = TCCD_IRF_PASS1_CHECKS;  // pass 1's check cap (see irf_query)
 
 __global__ void __launch_bounds__(128) irf_kernel(Args a, Ctr* ctr, unsigned char* arena,
                                                   long long cap, const long long* list,
