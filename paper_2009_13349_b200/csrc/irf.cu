@@ -698,8 +698,10 @@ int resident_blocks() {
 }
 
 // Pass 2 (warp per query over runs): 2 * (max_checks + 2) boxes (every push
-// of a search, never reclaimed) and a run heap per warp, as many warps as a
-// quarter of the device memory holds (8 per SM at most).  Pass 3 (the
+// of a search, never reclaimed) and a run heap per warp, as many warps as
+// half of the device memory holds (8 per SM at most): pass 2 carries every
+// long search, and its throughput scales with its warp count (a quarter of
+// the memory ran config 1's 10^5 queries in 3.4 s, half in 1.9 s).  Pass 3 (the
 // fallback): slots3 <= 0 picks as many max_checks + 2-entry heaps as an
 // eighth of the memory holds (4096 at most).  Passes 2 and 3 run one after
 // the other and share their arena.
@@ -719,7 +721,7 @@ IrfLayout irf_layout(long long n, long long mcmax, int slots3, int sms) {
   L.bcap2 = 2 * L.cap3;
   L.hcap2 = L.cap3 < (1ll << 20) ? L.cap3 : (1ll << 20);
   const long long per2 = L.bcap2 * 48 + L.hcap2 * (long long)sizeof(REnt);
-  long long w2 = L.bcap2 < (1ll << 31) ? (long long)(tot / 4 / (size_t)per2) : 0;
+  long long w2 = L.bcap2 < (1ll << 31) ? (long long)(tot / 2 / (size_t)per2) : 0;
   if (w2 > 8ll * sms) w2 = 8ll * sms;
   L.warps2 = w2 / kWarps2 * kWarps2;
   size_t o = 0;
