@@ -716,6 +716,7 @@ IrfLayout irf_layout(long long n, long long mcmax, int slots3, int sms) {
     s3 = (long long)(tot / 8 / ((size_t)L.cap3 * 64));
     if (s3 > 4096) s3 = 4096;
     if (s3 < sms) s3 = sms;
+    if (s3 > n) s3 = n > 0 ? n : 1;  // (no more slots than queries)
   }
   L.slots3 = (s3 + 31) / 32 * 32;
   L.bcap2 = 2 * L.cap3;
@@ -723,6 +724,7 @@ IrfLayout irf_layout(long long n, long long mcmax, int slots3, int sms) {
   const long long per2 = L.bcap2 * 48 + L.hcap2 * (long long)sizeof(REnt);
   long long w2 = L.bcap2 < (1ll << 31) ? (long long)(tot / 2 / (size_t)per2) : 0;
   if (w2 > 8ll * sms) w2 = 8ll * sms;
+  if (w2 > n + kWarps2 - 1) w2 = n + kWarps2 - 1;  // (no more warps than queries)
   L.warps2 = w2 / kWarps2 * kWarps2;
   size_t o = 0;
   L.ctr = o; o += a256(sizeof(Ctr));

@@ -66,7 +66,13 @@ def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
     key = (device.type, device.index)
     ws = _workspaces.get(key)
     if ws is None or ws.numel() < nbytes:
+        # drop the smaller cached workspace (and give its memory back) before
+        # allocating the larger one: both would not fit at ~100 GB sizes
         _workspaces.pop(key, None)
+        if ws is not None:
+            del ws
+            torch.cuda.synchronize(device)  # (work on the old one may be in flight)
+            torch.cuda.empty_cache()
         ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
         _workspaces[key] = ws
     return ws
