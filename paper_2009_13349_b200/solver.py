@@ -119,7 +119,9 @@ def _default_heavy_blocks(device: torch.device, n: int, max_checks_max: int) -> 
     free, _ = torch.cuda.mem_get_info(device)
     cached = sum(w.numel() for (t, i), w in _workspaces.items() if i == device.index)
     budget = (free + cached) // 2 - base
-    return max(1, min(sms, int(budget // per)))
+    # (no more giant-tier groups than queries: a small batch does not reserve
+    # 148 arenas of 2 * m_I boxes)
+    return max(1, min(sms, max(int(n), 1), int(budget // per)))
 
 
 def workspace_bytes(n: int, max_checks_max: int, heavy_blocks: int) -> int:
