@@ -50,6 +50,7 @@ __all__ = [
 
 _SQRT3 = math.sqrt(3.0)
 _DISTANCE_SLACK = 1e-9  # scene.py:42-45
+_LS_WINDOW = 1 << 18  # candidates per line-search solve
 
 
 def edges_from_triangles(triangles) -> np.ndarray:
@@ -571,15 +572,17 @@ def line_search_step(mesh: TriMeshPair, *, p: float, delta: float = 1e-6,
         bounds = []
         i0 = 0
         while i0 < m:
-            # candidates i0.. solved at the current alpha; results hold until
-            # the first one that lowers alpha
+            # a window of candidates i0.. solved at the current alpha; results
+            # hold up to the first one that lowers alpha, the rest are solved
+            # again at the new alpha (windows bound that repeated work)
+            i1 = min(m, i0 + _LS_WINDOW)
             cfg = SolverConfig(delta=tol_assumed, max_checks=max_checks, t_max=alpha)
-            r = _solve(cs, slice(i0, m), cfg, seps[i0:], device)
+            r = _solve(cs, slice(i0, i1), cfg, seps[i0:i1], device)
             hit = r["status"] == 1
             toi = r["toi"]
             lower = hit & (toi < alpha)
             lowered = bool(lower.any())
-            j_end = int(np.argmax(lower)) + 1 if lowered else m - i0
+            j_end = int(np.argmax(lower)) + 1 if lowered else i1 - i0
             # a free result carries codomain width 0 (solver.py:89-93)
             if j_end:
                 achieved = max(achieved, float(np.max(np.where(hit[:j_end], r["codom"][:j_end], 0.0))))
@@ -600,7 +603,7 @@ def line_search_step(mesh: TriMeshPair, *, p: float, delta: float = 1e-6,
                     else:
                         bounds.append(CandidateBound._trusted(cands[i0 + j], d_l[j], s_l[j],
                                                               None, None))
-            nxt = m
+            nxt = i1
             if lowered:
                 alpha = toi_l[j_end - 1]
                 limiting = len(bounds) - 1

@@ -199,6 +199,17 @@ def test_line_search_host_logic(tag, oracle_device):
         _check_ls(tag, p, infl, line_search_step(mesh, p=p, inflation=infl))
 
 
+@pytest.mark.parametrize("tag", TAGS)
+def test_line_search_windows(tag, oracle_device, monkeypatch):
+    """Candidates solved in windows of 7 (re-solving after every alpha
+    change, window by window) give the reference's results too."""
+    import paper_2009_13349_b200.scene as S
+    monkeypatch.setattr(S, "_LS_WINDOW", 7)
+    mesh = _mesh(tag)
+    for p, infl in LS_CASES:
+        _check_ls(tag, p, infl, line_search_step(mesh, p=p, inflation=infl))
+
+
 def test_line_search_energy_loop(oracle_device):
     mesh = _mesh("mover_free")
     calls = []
