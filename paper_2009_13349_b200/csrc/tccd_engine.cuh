@@ -337,11 +337,13 @@ struct EngineShared {
   unsigned long long sw[2 * (Cfg::G / 32)];
   int swi[4 * (Cfg::G / 32)];
   int any_general;
-  // one-query tier, dyadic t_max: every box of a level has the same widths,
-  // so a materialized box is stored as its lower corner (t0, u0, v0) only
-  double w[3];           // widths of the current level's boxes
-  double wp[3];          // widths of the previous level's (the parents')
-  int lvl_sdim;          // split dimension of the current level's refining boxes
+  // dyadic t_max: every box of a query's level has the same widths, so in a
+  // round whose resident queries are all dyadic a materialized box is stored
+  // as its lower corner (t0, u0, v0) only
+  double w[Q][3];        // widths of the current level's boxes
+  double wp[Q][3];       // widths of the previous level's (the parents')
+  int lvl_sdim[Q];       // split dimension of the current level's refining boxes
+  int allu;              // every resident query dyadic (this round's arrays compact)
   int n_cur, n_next, admit_k, exhausted, A_tot, B_tot, P_tot, rot;
   unsigned long long deferred;
   int deferred_last;     // queries deferred in the previous round
@@ -468,6 +470,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   if (tid == 0) { S.n_cur = 0; S.exhausted = 0; S.rot = 0; S.deferred = 0; S.deferred_last = 0; }
   gsync<G>();
   int cur = 0;
+  bool cprv = false;  // the previous round's level arrays are compact
   long long rounds = 0;
   unsigned long long evicted = 0, boxes = 0;
   unsigned int ncls_vf = 0, ncls_ee = 0;  // this thread's classifications per kind
@@ -532,6 +535,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         cnt += __popc(m);
       }
       if (tid == 0) {
+        S.allu = 1;
         int k = (int)cnt;
         int room = admit_lim - S.n_cur;
         if (room < 0) room = 0;
@@ -604,16 +608,15 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       S.uniform[s] = frexp(S.qp[s].t_max, &ex) == 0.5;  // t_max a power of two
       int nr = 1;
       long long off = -1;
-      if constexpr (ONEQ) {  // (root widths; a handed-over level's below)
-        S.w[0] = S.qp[s].t_max; S.w[1] = 1.0; S.w[2] = 1.0;
-      }
+      // (root widths; a handed-over level's below)
+      S.w[s][0] = S.qp[s].t_max; S.w[s][1] = 1.0; S.w[s][2] = 1.0;
       if (io.in_hand && io.in_hand[entry(S.admit_base + r)].n > 0) {
         const Hand& hd = io.in_hand[entry(S.admit_base + r)];
         nr = hd.n;
         off = hd.off;
-        if constexpr (ONEQ) {
+        {
           const Box pb = io.in_pbox[off];
-          S.w[0] = pb.t1 - pb.t0; S.w[1] = pb.u1 - pb.u0; S.w[2] = pb.v1 - pb.v0;
+          S.w[s][0] = pb.t1 - pb.t0; S.w[s][1] = pb.u1 - pb.u0; S.w[s][2] = pb.v1 - pb.v0;
         }
         S.C[s] = hd.C;
         S.level[s] = hd.level;
@@ -670,6 +673,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       S.acc[s] = kIntMax;
       S.cont[s] = 0;
       S.unsorted[s] = 0;
+      if (S.qidx[s] >= 0 && !S.uniform[s]) S.allu = 0;
     }
     gsync<G>();
     TCCD_PHASE(1);
@@ -695,16 +699,17 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     const int n1 = ONEQ ? (int)min((long long)n, S.seg_off[0] + max(S.qp[0].max_checks - S.C[0], 0ll))
                         : n;
     boxes += (unsigned long long)n1;
-    // compact boxes (one query, dyadic t_max): the level arrays hold lower
-    // corners; a parent (of the previous level) is completed with wp
-    const bool compact = ONEQ && S.uniform[0];
+    // compact boxes (every resident query dyadic): this round's level arrays
+    // hold lower corners; a box of the previous round's arrays (stored compact
+    // if cprv) is completed with its query's widths when it is used
+    const bool compact = S.allu != 0;
     const double* const cprev = reinterpret_cast<const double*>(bprev);
     double* const ccur = reinterpret_cast<double*>(bx);
     // load box r of the previous level or of the pool into o (a compact
     // parent only with its lower corner: completed when it is used)
     auto fetch = [&](unsigned int r, Box& o) {
       if (!(r & kRefRoot)) {
-        if (compact) {
+        if (cprv) {
           const double* q = cprev + 3 * (size_t)(r & kRefSrcMask);
           o.t0 = q[0]; o.u0 = q[1]; o.v0 = q[2];
         } else {
@@ -715,10 +720,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       }
     };
     // a box of the current level (compact: completed with the level's widths)
-    auto box_at = [&](int x) -> Box {
+    auto box_at = [&](int x, int s) -> Box {
       if (!compact) return bx[x];
       const double* q = ccur + 3 * (size_t)x;
-      return Box{q[0], q[0] + S.w[0], q[1], q[1] + S.w[1], q[2], q[2] + S.w[2]};
+      const double* w = S.w[s];
+      return Box{q[0], q[0] + w[0], q[1], q[1] + w[1], q[2], q[2] + w[2]};
     };
     unsigned int r_cur = tid < n1 ? rf[tid] : kRefRoot;
     Box p_cur;
@@ -745,10 +751,6 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       const unsigned int r_nn = i + 2 * NT < n1 ? rf[i + 2 * NT] : kRefRoot;
       const unsigned int r = r_cur;
       Box p = p_cur;
-      if (compact && !(r & kRefRoot)) {  // complete the parent (or the box itself)
-        const double* wq = (r & kRefSelf) ? S.w : S.wp;
-        p.t1 = p.t0 + wq[0]; p.u1 = p.u0 + wq[1]; p.v1 = p.v0 + wq[2];
-      }
       const uint8_t pf = pf_cur;
       pf_cur = pf_nxt;
       r_cur = r_nxt;
@@ -758,6 +760,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       if (i < n1) {
       const int s = ONEQ ? 0 : sl[i];
       const QueryParams& qp = S.qp[s];
+      if (cprv && !(r & kRefRoot)) {  // complete the parent (or the box itself)
+        const double* wq = (r & kRefSelf) ? S.w[s] : S.wp[s];
+        p.t1 = p.t0 + wq[0]; p.u1 = p.u0 + wq[1]; p.v1 = p.v0 + wq[2];
+      }
       Box b;
       f = Cfg::SMEM ? fl[i] : f_pre;  // head bit (+ class, for roots and deferred boxes)
       double wb = 0.0;
@@ -814,12 +820,12 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         if (compact) {
           double* q = ccur + 3 * (size_t)i;
           q[0] = b.t0; q[1] = b.u0; q[2] = b.v0;
-          // (classified here or carried, e.g. the root's: the same for every
-          // refining box of the level)
-          if (!(f & 4)) S.lvl_sdim = (f >> 3) & 3;
         } else {
           bx[i] = b;
         }
+        // (classified here or carried, e.g. the root's: the same for every
+        // refining box of a dyadic query's level)
+        if (!(f & 4)) S.lvl_sdim[s] = (f >> 3) & 3;
         wbc[i] = wb;
         atomicMin(&S.j[s], k);
         // first accepted box: if it is not j itself it lies after j, and it is
@@ -868,7 +874,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         }
       } else {
         const int ij = S.seg_off[s] + j;
-        const Box bj = box_at(ij);
+        const Box bj = box_at(ij, s);
         const double wbj = wbc[ij];
         Rec& fr = S.rec[s][0];
         fr.b = bj;
@@ -889,7 +895,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           const long long eend = nn < cut ? nn : cut;
           const int ai = S.acc[s];
           if (ai < eend) {
-            const Box ba = box_at(S.seg_off[s] + ai);
+            const Box ba = box_at(S.seg_off[s] + ai, s);
             if (!S.have_drop[s] || ba.t0 < S.rec[s][1].b.t0) {
               Rec& dr = S.rec[s][1];
               dr.b = ba;
@@ -1239,7 +1245,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         } else {
           // materialize the handed-over level in the next tier's pool
           const long long base = S.hoff[s];
-          const Box pb = bx[i];
+          const Box pb = box_at(i, s);
           double mid;
           const int sd = split_dim(pb, S.qp[s].kap, mid);
           Box c0, c1;
@@ -1264,7 +1270,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       const uint8_t f = fl[i];
       if ((f & 3) == kDisjoint || (f & 4)) continue;
       const int sdim = (f >> 3) & 3;
-      const Box b = bx[i];
+      const Box b = box_at(i, ONEQ ? 0 : sl[i]);
       const int c = i >> 5;
       const unsigned int lm = lowmask(i & 31);
       const unsigned int oa = (unsigned)(ch.c[kCA][c] + __popc(ch.m[kMR][c] & lm) +
@@ -1350,7 +1356,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           sln[pos] = (uint8_t)s;
           fln[pos] = 0;
         } else {
-          const Box pb = bx[r & kRefSrcMask];
+          const Box pb = box_at(r & kRefSrcMask, s);
           double mid;
           const int sd = split_dim(pb, S.qp[s].kap, mid);
           Box c0, c1;
@@ -1370,9 +1376,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         S.seg_n[s] = S.tot[s];
         S.level[s] += 1;
         S.seg_off[s] = S.next_off[s];
-        if (compact) {  // the next level's boxes: this level's split dimension halved
-          S.wp[0] = S.w[0]; S.wp[1] = S.w[1]; S.wp[2] = S.w[2];
-          S.w[S.lvl_sdim] = 0.5 * S.w[S.lvl_sdim];
+        if (S.uniform[s]) {  // the next level's boxes: this level's split dimension halved
+          double* w = S.w[s];
+          S.wp[s][0] = w[0]; S.wp[s][1] = w[1]; S.wp[s][2] = w[2];
+          w[S.lvl_sdim[s]] = 0.5 * w[S.lvl_sdim[s]];
         }
       } else if (S.cont[s] == 2) {
         S.C[s] -= S.seg_n[s];  // the level re-runs next round
@@ -1383,6 +1390,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     TCCD_PHASE(9);
     if (tid == 0) S.n_cur = S.n_next;
     cur = nxt;
+    cprv = compact;
     gsync<G>();
     TCCD_PHASE(10);
   }
