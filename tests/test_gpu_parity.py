@@ -97,6 +97,24 @@ def test_mixed_dyadic_and_general_t_max(cuda, config, start, count):
     _vs_oracle(w, cuda, t_max=t_max)
 
 
+@pytest.mark.parametrize("config,start,count,frac", [(1, 90_000, 40_000, 0.03),
+                                                     (1, 130_000, 40_000, 0.2),
+                                                     (3, 200_000, 100_000, 0.01)])
+def test_compact_format_switches(cuda, config, start, count, frac):
+    """Mostly dyadic t_max with a few non-dyadic queries: a group stores its
+    level arrays as lower corners only in rounds whose resident queries are
+    all dyadic, so admitting a non-dyadic query (or finishing the last one)
+    switches the format between rounds, with deferred and handed-over levels
+    read across the switch."""
+    from paper_2009_13349_b200 import workloads as W
+    w = W.generate(config, start, count)
+    rng = np.random.default_rng(config + 91)
+    t_max = rng.choice(np.array([1.0, 0.5, 0.25]), count)
+    odd = rng.random(count) < frac
+    t_max[odd] = rng.choice(np.array([0.3, 0.7, 0.9]), int(odd.sum()))
+    _vs_oracle(w, cuda, t_max=t_max)
+
+
 def test_extreme_coordinates_nan_path(cuda):
     """Coordinates near the top of the binary64 range: lerps and corner values
     overflow to +-inf and inf - inf = NaN.  The reference's hull ignores NaN
