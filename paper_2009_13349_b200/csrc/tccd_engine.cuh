@@ -61,6 +61,9 @@ constexpr int kIntMax = 0x7fffffff;
 #endif
 constexpr uint8_t kClassified = 64;  // flag bit: box already classified
 constexpr uint8_t kHead = 128;       // flag bit: first box of a run of equal t_lo
+// P4c modes of a slot: children kept here (closed form), level carried
+// (deferred), children handed over to the next tier's pool (closed form)
+constexpr uint8_t kPcKeep = 1, kPcCarry = 2, kPcHand = 3;
 
 // reference encoding
 constexpr unsigned kRefSrcMask = (1u << 29) - 1;  // position in the previous box array
@@ -337,6 +340,8 @@ struct EngineShared {
   unsigned long long sw[2 * (Cfg::G / 32)];
   int swi[4 * (Cfg::G / 32)];
   int any_general;
+  int4 pc[Q];            // P4c view of a slot: next offset, segment P0 (or offset), P1, A0
+  uint8_t pc_mode[Q];    // P4c: 0 skip, kPcKeep, kPcCarry, kPcHand
   // dyadic t_max: every box of a query's level has the same widths, so in a
   // round whose resident queries are all dyadic a materialized box is stored
   // as its lower corner (t0, u0, v0) only
@@ -1112,6 +1117,22 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         S.deferred += deferred;
         S.deferred_last = deferred;
       }
+      if constexpr (!ONEQ) {
+        // P4c's per-slot view, one 16-byte word and a mode byte per slot
+#pragma unroll
+        for (int m = 0; m < kPer; ++m) {
+          const int s = vslot(lane * kPer + m);
+          if (s < 0) continue;
+          const int cs = S.cont[s];
+          uint8_t md = 0;
+          if (cs == 2) md = kPcCarry;
+          else if (S.uniform[s] && cs == 1) md = kPcKeep;
+          else if (S.uniform[s] && cs == 3 && S.hoff[s] >= 0) md = kPcHand;
+          S.pc_mode[s] = md;
+          if (md) S.pc[s] = make_int4(cs == 3 ? 0 : S.next_off[s], cs == 2 ? S.seg_off[s] : S.segP0[s],
+                                      S.segP1[s], S.segA0[s]);
+        }
+      }
     }
     gsync<G>();
     TCCD_PHASE(7);
@@ -1179,6 +1200,73 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
             if (ru >= 0) {
               outr[base + ru] = (unsigned)i | kRefCb;
               fln[base + ru] = tsplit ? hd : 0;
+            }
+          }
+        }
+      } else if constexpr (!ONEQ) {
+        // lane per box; the slot's view is one 16-byte word (pc) and a mode
+        for (int i = tid; i < n; i += NT) {
+          const int c = i >> 5, l = i & 31;
+          const unsigned int lm = lowmask(l), bit = 1u << l;
+          const unsigned int R = ch.m[kMR][c];
+          if (!any_deferred && !(R & bit)) continue;
+          const int s = sl[i];
+          const int md = S.pc_mode[s];
+          if (md == 0) continue;
+          const int4 pv = S.pc[s];
+          if (md == kPcCarry) {
+            const int pos = pv.x + (i - pv.y);
+            TCCD_ASSERT(pos < cap);
+            outr[pos] = (unsigned)i | kRefSelf;
+            sln[pos] = (uint8_t)s;
+            fln[pos] = fl[i];
+            continue;
+          }
+          if (!(R & bit)) continue;
+          const unsigned int H = ch.m[kMH][c], T = ch.m[kMT][c], U = ch.m[kMU][c];
+          const int cP = ch.c[kCP][c], cM = ch.c[kCM][c], cN = ch.c[kCN][c], cA = ch.c[kCA][c];
+          const int Pr = cP + __popc(R & lm);
+          const unsigned int hle = H & (lm | bit), hgt = H & ~(lm | bit);
+          const int M = hle ? cP + __popc(R & lowmask(31 - __clz(hle))) : cM;
+          int N = hgt ? cP + __popc(R & lowmask(__ffs(hgt) - 1)) : cN;
+          if (N > pv.z) N = pv.z;  // the last run ends at the segment end
+          const int S0 = pv.y;
+          const bool tsplit = (T & bit) != 0;
+          const uint8_t hd = Pr == M ? kHead : 0;
+          int rl, ru = -1;
+          if (tsplit) {
+            rl = (M - S0) + (Pr - S0);
+            ru = (N - S0) + (Pr - S0);
+          } else {
+            rl = cA + __popc(R & lm) + __popc(U & lm) - pv.w;
+            if (U & bit) ru = rl + 1;
+          }
+          const uint8_t hu = tsplit ? hd : 0;
+          if (md == kPcKeep) {
+            const int base = pv.x;
+            TCCD_ASSERT(base + rl < cap && base + ru < cap);
+            outr[base + rl] = (unsigned)i;
+            sln[base + rl] = (uint8_t)s;
+            fln[base + rl] = hd;
+            if (ru >= 0) {
+              outr[base + ru] = (unsigned)i | kRefCb;
+              sln[base + ru] = (uint8_t)s;
+              fln[base + ru] = hu;
+            }
+          } else {
+            // materialize the handed-over level in the next tier's pool
+            const long long base = S.hoff[s];
+            const Box pb = box_at(i, s);
+            double mid;
+            const int sd = split_dim(pb, S.qp[s].kap, mid);
+            Box c0, c1;
+            children(pb, sd, mid, c0, c1);
+            TCCD_ASSERT(base + rl < io.pool_cap && base + ru < io.pool_cap);
+            io.out_pbox[base + rl] = c0;
+            io.out_pflag[base + rl] = hd;
+            if (ru >= 0) {
+              io.out_pbox[base + ru] = c1;
+              io.out_pflag[base + ru] = hu;
             }
           }
         }
