@@ -324,7 +324,8 @@ struct EngineShared {
   double root_wb[Q];
   int level[Q];
   int seg_off[Q], seg_n[Q];
-  int j[Q], acc[Q];
+  int j[Q], acc[Q];       // P1: flat position of the first non-disjoint / accepted box
+  int cutpos[Q];         // flat position of the segment's last box within the budget
   int segA0[Q], segB0[Q], segA1[Q], segB1[Q];
   int next_off[Q];
   int tot[Q];
@@ -678,7 +679,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       S.acc[s] = kIntMax;
       S.cont[s] = 0;
       S.unsorted[s] = 0;
-      if (S.qidx[s] >= 0 && !S.uniform[s]) S.allu = 0;
+      if (S.qidx[s] >= 0) {
+        if (!S.uniform[s]) S.allu = 0;
+        const long long cp = S.seg_off[s] + (S.qp[s].max_checks - S.C[s] - 1);
+        S.cutpos[s] = (int)max(min(cp, (long long)kIntMax - 1), -1ll);
+      }
     }
     gsync<G>();
     TCCD_PHASE(1);
@@ -801,10 +806,8 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           if (up) b.v0 = mid; else b.v1 = mid;
         }
       }
-      const int k = i - S.seg_off[s];
       if (!(f & kClassified)) {
-        const long long cut = qp.max_checks - S.C[s] - 1;
-        if (k <= cut) {
+        if (i <= S.cutpos[s]) {
           const uint8_t head = f & kHead;
           const int cls = classify((const double*)S.P[s], qp.kind, b, qp.eps, qp.sep, wb, qp.tame != 0);
           ncls_ee += qp.kind;  // (kind is 0 or 1)
@@ -832,10 +835,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         // refining box of a dyadic query's level)
         if (!(f & 4)) S.lvl_sdim[s] = (f >> 3) & 3;
         wbc[i] = wb;
-        atomicMin(&S.j[s], k);
+        atomicMin(&S.j[s], i);
         // first accepted box: if it is not j itself it lies after j, and it is
         // the only candidate for the drop record (boxes are in t_lo order)
-        if (f & 4) atomicMin(&S.acc[s], k);
+        if (f & 4) atomicMin(&S.acc[s], i);
       }
       fl[i] = f;
       }  // i < n
@@ -865,7 +868,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       const long long C = S.C[s], mc = S.qp[s].max_checks;
       const long long cut = mc - C - 1;
       const long long ecls = nn < cut + 1 ? nn : cut + 1;
-      const int j = S.j[s];
+      const int j = S.j[s] == kIntMax ? kIntMax : S.j[s] - S.seg_off[s];  // (segment-relative)
       bool done = true;
       if (j >= ecls) {
         if (cut < nn) {
@@ -898,7 +901,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           }
         } else {
           const long long eend = nn < cut ? nn : cut;
-          const int ai = S.acc[s];
+          const int ai = S.acc[s] == kIntMax ? kIntMax : S.acc[s] - S.seg_off[s];
           if (ai < eend) {
             const Box ba = box_at(S.seg_off[s] + ai, s);
             if (!S.have_drop[s] || ba.t0 < S.rec[s][1].b.t0) {
