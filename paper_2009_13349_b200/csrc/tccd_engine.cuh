@@ -150,7 +150,7 @@ __device__ __forceinline__ void group_excl_scan2(unsigned long long v0, unsigned
     e1 = (w ? sw[NW + w - 1] : 0ull) + x1 - v1;
     t0 = sw[NW - 1];
     t1 = sw[2 * NW - 1];
-    __syncthreads();
+    // (no trailing barrier: the caller's next write to sw is behind one)
   }
 }
 
@@ -199,7 +199,7 @@ __device__ __forceinline__ void group_scan_maxfwd_minrev(int vm, int vn, int* sw
     __syncthreads();
     em = max(swi[2 * NW + w], exm);
     en = min(swi[3 * NW + w], exn);
-    __syncthreads();
+    // (no trailing barrier: the caller's next write to swi is behind one)
   }
 }
 
