@@ -341,8 +341,8 @@ struct EngineShared {
   unsigned long long sw[2 * (Cfg::G / 32)];
   int swi[4 * (Cfg::G / 32)];
   int any_general;
-  int4 pc[Q];            // P4c view of a slot: next offset, segment P0 (or offset), P1, A0
-  uint8_t pc_mode[Q];    // P4c: 0 skip, kPcKeep, kPcCarry, kPcHand
+  int4 pc[Q];            // P4c view of a slot: next offset, segment P0 (carry: offset), P1, A0
+  uint8_t pc_mode[Q];    // P4c: 0 skip, kPcKeep, kPcCarry, kPcHand (set where decided)
   // dyadic t_max: every box of a query's level has the same widths, so in a
   // round whose resident queries are all dyadic a materialized box is stored
   // as its lower corner (t0, u0, v0) only
@@ -513,6 +513,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       hd.have_drop = S.have_drop[s];
     }
     S.hoff[s] = off;
+    if (off >= 0 && S.uniform[s]) S.pc_mode[s] = kPcHand;
     S.qidx[s] = -1;
     S.cont[s] = 3;
     ++evicted;
@@ -679,6 +680,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       S.acc[s] = kIntMax;
       S.cont[s] = 0;
       S.unsorted[s] = 0;
+      S.pc_mode[s] = 0;
       if (S.qidx[s] >= 0) {
         if (!S.uniform[s]) S.allu = 0;
         const long long cp = S.seg_off[s] + (S.qp[s].max_checks - S.C[s] - 1);
@@ -1019,6 +1021,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           prefix(S.seg_off[s] + S.seg_n[s], a1, b1, p1);
           S.segA0[s] = a0; S.segB0[s] = b0; S.segP0[s] = p0;
           S.segA1[s] = a1; S.segB1[s] = b1; S.segP1[s] = p1;
+          S.pc[s] = make_int4(0, p0, p1, a0);
           t = (a1 - a0) + (b1 - b0);
           if (!S.uniform[s]) S.any_general = 1;
           if (t > qcap) evict(s, t);
@@ -1103,8 +1106,13 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         if (s >= 0 && S.cont[s] == 1) {
           if (rpos < K) {
             S.next_off[s] = ut;
+            S.pc[s].x = ut;
+            if (S.uniform[s]) S.pc_mode[s] = kPcKeep;
           } else {
             S.next_off[s] = cT + (un - cN);
+            S.pc[s].x = cT + (un - cN);
+            S.pc[s].y = S.seg_off[s];
+            S.pc_mode[s] = kPcCarry;
             S.cont[s] = 2;
             ++deferred;
           }
@@ -1119,22 +1127,6 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         S.rot = (S.rot + 1) % Q;
         S.deferred += deferred;
         S.deferred_last = deferred;
-      }
-      if constexpr (!ONEQ) {
-        // P4c's per-slot view, one 16-byte word and a mode byte per slot
-#pragma unroll
-        for (int m = 0; m < kPer; ++m) {
-          const int s = vslot(lane * kPer + m);
-          if (s < 0) continue;
-          const int cs = S.cont[s];
-          uint8_t md = 0;
-          if (cs == 2) md = kPcCarry;
-          else if (S.uniform[s] && cs == 1) md = kPcKeep;
-          else if (S.uniform[s] && cs == 3 && S.hoff[s] >= 0) md = kPcHand;
-          S.pc_mode[s] = md;
-          if (md) S.pc[s] = make_int4(cs == 3 ? 0 : S.next_off[s], cs == 2 ? S.seg_off[s] : S.segP0[s],
-                                      S.segP1[s], S.segA0[s]);
-        }
       }
     }
     gsync<G>();
