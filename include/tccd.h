@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TCCD_ABI_VERSION 2
+#define TCCD_ABI_VERSION 3
 
 /* Per-query status values written to tccd_batch.status. */
 #define TCCD_STATUS_FREE 0           /* certified collision free, toi = +inf   */
@@ -62,6 +62,51 @@ extern "C" {
 /* flags */
 #define TCCD_FLAG_HEAVY_ONLY 1u /* route every query through the block-per-query
                                    engine (testing / diagnostics)             */
+#define TCCD_FLAG_NO_LANE 2u    /* skip the lane tier: every survivor of the
+                                   root check goes through the group tiers
+                                   (testing / diagnostics)                    */
+
+/* Solver stages, in launch order per chunk (tccd_batch.events). */
+#define TCCD_STAGE_PROLOGUE 0 /* validation, filters, kappas, root check     */
+#define TCCD_STAGE_LANE 1     /* thread-per-query tier (dyadic t_max)        */
+#define TCCD_STAGE_LIGHT 2    /* group tiers: light, medium, giant           */
+#define TCCD_STAGE_MEDIUM 3
+#define TCCD_STAGE_GIANT 4
+#define TCCD_NUM_STAGES 5
+
+/* Diagnostic counters (tccd_batch.stats, TCCD_NUM_STATS int64, summed over
+ * chunks). */
+#define TCCD_NUM_STATS 32
+#define TCCD_STAT_GIANT_QUERIES 0   /* queries that reached the giant tier      */
+#define TCCD_STAT_ROUNDS 1          /* group-engine rounds                      */
+#define TCCD_STAT_DEFERRALS 2       /* group-engine level deferrals             */
+#define TCCD_STAT_MEDIUM_QUERIES 3  /* queries that reached the medium tier     */
+#define TCCD_STAT_BOXES 4           /* [4..6] boxes visited per group tier      */
+#define TCCD_STAT_LANE_QUERIES 7    /* queries that entered the lane tier       */
+#define TCCD_STAT_CLS 8             /* [8..13] box classifications per group
+                                       tier and kind (light VF, light EE, medium
+                                       VF, medium EE, giant VF, giant EE)       */
+#define TCCD_STAT_LANE_CLS 14       /* [14..15] lane classifications VF, EE     */
+#define TCCD_STAT_LANE_CHECKS 16    /* [16..17] checks of the queries the lane
+                                       tier finished, root check excluded (the
+                                       prologue's): the reference's own count,
+                                       so algorithmic work                      */
+#define TCCD_STAT_LANE_DONE 18      /* [18..19] queries the lane tier finished  */
+#define TCCD_STAT_LANE_EVICTED 20   /* queries the lane tier sent to the light
+                                       tier (restart from the root)             */
+#define TCCD_STAT_LANE_WASTED 21    /* lane checks of those queries             */
+#define TCCD_STAT_POOL_DEMAND 22    /* [22..23] handover boxes requested light->
+                                       medium, medium->giant                    */
+#define TCCD_STAT_RESTARTS 24       /* [24..25] evictions light->medium,
+                                       medium->giant that found the handover
+                                       pool full (restart from the root)        */
+#define TCCD_STAT_TIER_CHECKS 26    /* [26..28] checks of the reference's path
+                                       done in the light, medium, giant tiers
+                                       (classifications past a query's return
+                                       point, deferral re-runs and restarted
+                                       work excluded)                           */
+#define TCCD_STAT_PROLOGUE_DONE 29  /* queries decided at the root (or invalid) */
+#define TCCD_STAT_CHUNKS 31         /* library chunks ([30] reserved)           */
 
 /*
  * One batched solve.  All array pointers are DEVICE pointers.  For every
@@ -114,25 +159,38 @@ typedef struct tccd_batch {
   size_t workspace_bytes;
   int32_t heavy_blocks; /* concurrent block-per-query solvers; 0 = default   */
   int32_t device_sms;   /* SM count of the target device; 0 = query it      */
-  int64_t *stats;       /* optional device [16] diagnostics: [0] queries
-                           that reached the giant tier, [1] engine rounds,
-                           [2] level deferrals, [3] queries that reached the
-                           medium tier, [4..6] boxes visited per tier
-                           (light, medium, giant), [7] reserved, [8..13]
-                           box classifications per tier and kind (light
-                           VF, light EE, medium VF, medium EE, giant VF,
-                           giant EE), [14..15] reserved                  */
-  void *const *events;  /* optional host array of 4 cudaEvent_t (NULL
-                           entries skipped), recorded on `stream` after the
-                           prologue, light, medium and giant stages of each
-                           4M-query chunk: per-kernel timing on the
-                           launching stream (ABI 2)                       */
+  int64_t *stats;       /* optional device [TCCD_NUM_STATS] diagnostics
+                           (TCCD_STAT_*)                                  */
+  void *const *events;  /* optional host array of TCCD_NUM_STAGES
+                           cudaEvent_t (NULL entries skipped), recorded on
+                           `stream` after each stage of each chunk:
+                           per-kernel timing on the launching stream     */
+  /* Optional compacted hit list (ABI 3): every query with status HIT
+   * appends (index, toi) -- in no particular order -- at position
+   * *hit_count (device u64, NOT reset by the call: zero it once and several
+   * calls append to one list), which ends as the number of entries written
+   * so far; it may exceed hit_capacity (entries past the capacity are
+   * dropped). */
+  int64_t *hit_index;
+  double *hit_toi;
+  uint64_t *hit_count;
+  int64_t hit_capacity;
+  int64_t hit_index_base; /* added to every index written to hit_index (a
+                             caller solving a slice of a larger batch)   */
+  int64_t pool_boxes;   /* handover pool boxes per tier transition and
+                           chunk; 0 = default (tccd_workspace_bytes must
+                           be asked with the same value: see
+                           tccd_workspace_bytes_ex)                      */
+  int64_t launches;     /* out: kernels this call launched               */
 } tccd_batch;
 
 /* Bytes of device workspace tccd_solve_batch needs for a batch of n queries
  * whose largest check budget is max_checks_max, with heavy_blocks concurrent
  * block-per-query solvers (0 = default for the current device). */
 size_t tccd_workspace_bytes(int64_t n, int64_t max_checks_max, int32_t heavy_blocks);
+/* The same for a non-default handover pool size (tccd_batch.pool_boxes). */
+size_t tccd_workspace_bytes_ex(int64_t n, int64_t max_checks_max, int32_t heavy_blocks,
+                               int64_t pool_boxes);
 
 /* Enqueue a batched solve on `stream` (cudaStream_t, NULL = legacy default).
  * Returns TCCD_OK or a TCCD_E_* code; per-query failures go to status[]. */
@@ -141,8 +199,10 @@ int tccd_solve_batch(const tccd_batch *batch, void *stream);
 /* Drop-in for _kernel.solve_kernel(s, e, kind, t_max, delta, max_checks,
  * sep, ex, ey, ez) (_kernel.py:136): HOST pointers s[4][3], e[4][3];
  * out13 receives (status, toi, tol, codom, checks, early, w_t0, w_t1, w_u0,
- * w_u1, w_v0, w_v1, w_level) as doubles.  Synchronous; allocates its own
- * device scratch (convenience path, not the throughput path). */
+ * w_u1, w_v0, w_v1, w_level) as doubles.  Synchronous, on the current
+ * device; its device scratch is cached per device and grows with the
+ * largest max_checks seen (no allocation per call once warm).  Calls are
+ * serialized by a library lock.  tccd_release_cached() frees the caches. */
 int tccd_solve_kernel(const double *s, const double *e, int kind, double t_max,
                       double delta, int64_t max_checks, double sep, double ex,
                       double ey, double ez, double *out13);
@@ -205,6 +265,18 @@ int tccd_irf_batch(const tccd_batch *batch, void *stream);
  * TCCD_E_CUDA if it is not, so the caller can fall back to cudaMemcpyAsync.
  */
 int tccd_copy_to_host(const void *src, void *host_dst, int64_t bytes, void *stream);
+
+void tccd_release_cached(void);
+
+/* Copy the first min(*count, max_elems) elements of elem_bytes each from
+ * device array src to pinned host memory, where *count (device) was written
+ * by an earlier kernel on `stream` (a compacted hit list, tccd_batch.
+ * hit_count): only the live entries cross the bus, with no host
+ * synchronization.  *count itself goes to host_count (pinned, may be NULL).
+ * A kernel on `stream` (see tccd_copy_to_host). */
+int tccd_copy_counted_to_host(const void *src, void *host_dst, int64_t elem_bytes,
+                              const uint64_t *count, int64_t max_elems, void *host_count,
+                              void *stream);
 
 const char *tccd_error_string(int code);
 int tccd_abi_version(void);

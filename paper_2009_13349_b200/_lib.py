@@ -13,8 +13,32 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TCCD_LIB") or os.path.join(_HERE, "libtccd.so")  # override: experiments only
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 FLAG_HEAVY_ONLY = 1
+FLAG_NO_LANE = 2
+
+# solver stages per chunk, in launch order (TCCD_STAGE_*)
+STAGES = ("prologue", "lane", "light", "medium", "giant")
+
+# diagnostic counters (TCCD_STAT_*, include/tccd.h)
+NUM_STATS = 32
+STAT_GIANT_QUERIES = 0
+STAT_ROUNDS = 1
+STAT_DEFERRALS = 2
+STAT_MEDIUM_QUERIES = 3
+STAT_BOXES = 4          # [4..6]
+STAT_LANE_QUERIES = 7
+STAT_CLS = 8            # [8..13]
+STAT_LANE_CLS = 14      # [14..15]
+STAT_LANE_CHECKS = 16   # [16..17]
+STAT_LANE_DONE = 18     # [18..19]
+STAT_LANE_EVICTED = 20
+STAT_LANE_WASTED = 21
+STAT_POOL_DEMAND = 22   # [22..23]
+STAT_RESTARTS = 24      # [24..25]
+STAT_TIER_CHECKS = 26   # [26..28]
+STAT_PROLOGUE_DONE = 29
+STAT_CHUNKS = 31
 
 STATUS_FREE = 0
 STATUS_HIT = 1
@@ -60,6 +84,13 @@ class TccdBatch(ctypes.Structure):
         ("device_sms", ctypes.c_int32),
         ("stats", _vp),
         ("events", _vp),
+        ("hit_index", _vp),
+        ("hit_toi", _vp),
+        ("hit_count", _vp),
+        ("hit_capacity", ctypes.c_int64),
+        ("hit_index_base", ctypes.c_int64),
+        ("pool_boxes", ctypes.c_int64),
+        ("launches", ctypes.c_int64),
     ]
 
 
@@ -83,12 +114,15 @@ EXPORTS = (
     "tccd_abi_version",
     "tccd_error_string",
     "tccd_workspace_bytes",
+    "tccd_workspace_bytes_ex",
     "tccd_solve_batch",
     "tccd_solve_kernel",
     "tccd_broad_create",
     "tccd_broad_emit",
     "tccd_broad_destroy",
     "tccd_copy_to_host",
+    "tccd_copy_counted_to_host",
+    "tccd_release_cached",
     "tccd_irf_workspace_bytes",
     "tccd_irf_batch",
 )
@@ -116,6 +150,11 @@ def lib() -> ctypes.CDLL:
         L.tccd_error_string.argtypes = [ctypes.c_int]
         L.tccd_workspace_bytes.restype = ctypes.c_size_t
         L.tccd_workspace_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32]
+        L.tccd_workspace_bytes_ex.restype = ctypes.c_size_t
+        L.tccd_workspace_bytes_ex.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                              ctypes.c_int64]
+        L.tccd_release_cached.restype = None
+        L.tccd_release_cached.argtypes = []
         L.tccd_solve_batch.restype = ctypes.c_int
         L.tccd_solve_batch.argtypes = [ctypes.POINTER(TccdBatch), _vp]
         L.tccd_solve_kernel.restype = ctypes.c_int
@@ -136,6 +175,9 @@ def lib() -> ctypes.CDLL:
         L.tccd_irf_batch.argtypes = [ctypes.POINTER(TccdBatch), _vp]
         L.tccd_copy_to_host.restype = ctypes.c_int
         L.tccd_copy_to_host.argtypes = [_vp, _vp, ctypes.c_int64, _vp]
+        L.tccd_copy_counted_to_host.restype = ctypes.c_int
+        L.tccd_copy_counted_to_host.argtypes = [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
+                                                _vp, _vp]
         v = L.tccd_abi_version()
         if v != ABI_VERSION:
             raise RuntimeError(f"libtccd ABI {v} != expected {ABI_VERSION}")

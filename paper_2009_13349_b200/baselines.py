@@ -18,7 +18,7 @@ import torch
 
 from . import _lib
 from .core import CCDResult, DomainBox, Query
-from .solver import _param, _ptr, _workspace, sm_count
+from .solver import _param, _ptr, _workspace, _workspace_guard, _workspace_release, sm_count
 
 # max_checks=None (the reference's unbounded search) runs with this budget on
 # the GPU; a query that spends it raises instead of returning a different
@@ -92,8 +92,10 @@ def irf_batch(points, kind, delta=1e-6, max_checks=1_000_000, t_max=1.0, *, devi
         b.workspace_bytes = ws.numel()
         b.heavy_blocks = slots
         b.device_sms = sm_count(dev)
-        rc = L.tccd_irf_batch(ctypes.byref(b),
-                              ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+        stream = torch.cuda.current_stream(dev)
+        _workspace_guard(dev, stream)
+        rc = L.tccd_irf_batch(ctypes.byref(b), ctypes.c_void_p(stream.cuda_stream))
+        _workspace_release(dev, stream)
         if rc == 3:
             raise ValueError("delta must be positive")
         if rc == 5:

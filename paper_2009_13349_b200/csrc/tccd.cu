@@ -27,10 +27,16 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <mutex>
 #include <type_traits>
+
+#include <cooperative_groups.h>
 
 #include "tccd.h"
 #include "tccd_device.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace tccd {
 
@@ -44,6 +50,14 @@ struct Counters {
   unsigned long long pool[3];     // handover pool fill (tiers 1, 2)
   unsigned long long phase[3][16];  // cycles per engine phase (TCCD_PHASE_PROF builds)
   unsigned long long cls[3][2];   // box classifications per tier and kind (VF, EE)
+  unsigned long long lane_count[2];  // lane-tier queue entries per kind (VF, EE)
+  unsigned long long lane_next[2];   // next lane entry to take per kind
+  // lane tier: [0..1] classifications VF / EE, [2..3] checks of the queries
+  // it finished (root check excluded: the prologue's), [4..5] queries
+  // finished, [6] queries evicted to the light tier, [7] their lane checks
+  unsigned long long lane[8];
+  unsigned long long restarts[3];  // evictions out of tier k that found the handover pool full
+  unsigned long long algo[3];      // checks of the reference's path done per group tier (signed sum)
 };
 
 // A queued query, self-contained so a tier admits it with one coalesced
@@ -103,6 +117,12 @@ struct Args {
   long long* stats;
   Counters* ctr;
   int heavy_only;
+  int no_lane;
+  long long* hit_index;    // optional compacted hit list (index, toi)
+  double* hit_toi;
+  unsigned long long* hit_count;
+  long long hit_cap;
+  long long hit_base;
 };
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -112,6 +132,17 @@ __device__ __forceinline__ void write_result(const Args& a, long long q, uint8_t
                                              int early, int level) {
   a.status[q] = status;
   const bool hit = status == kHit;
+  if (hit && a.hit_index) {
+    // compacted hit list: one atomic per group of converged hitting threads
+    const cg::coalesced_group g = cg::coalesced_threads();
+    unsigned long long base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(a.hit_count, (unsigned long long)g.size());
+    base = g.shfl(base, 0) + g.thread_rank();
+    if ((long long)base < a.hit_cap) {
+      a.hit_index[base] = q + a.hit_base;
+      a.hit_toi[base] = b.t0;
+    }
+  }
   a.toi[q] = hit ? b.t0 : __longlong_as_double(0x7ff0000000000000LL);
   if (a.tol) a.tol[q] = hit ? b.t1 - b.t0 : 0.0;
   if (a.codom) a.codom[q] = hit ? codom : 0.0;
@@ -132,6 +163,12 @@ __device__ __forceinline__ void load_params(const Args& a, long long q, QueryPar
   qp.sep = a.sep ? a.sep[q] : a.sep_all;
   qp.t_max = a.t_max ? a.t_max[q] : a.t_max_all;
 }
+
+}  // namespace tccd
+
+#include "tccd_lane.cuh"
+
+namespace tccd {
 
 // flag byte: bits 0-1 class, bit 2 accepted, bits 3-4 split dim, bit 5 upper
 // child pushed, bit 6 classified
@@ -181,7 +218,9 @@ constexpr int kPrologueThreads = 128;
 
 __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long long lo,
                                                                     long long cnt, Pre* queue,
-                                                                    unsigned long long* qcount) {
+                                                                    unsigned long long* qcount,
+                                                                    LaneRec* lq, long long lq_cap,
+                                                                    unsigned long long* lcount) {
   __shared__ double tile[kPrologueThreads * 24];
   const long long base = lo + (long long)blockIdx.x * kPrologueThreads;
   const int nb = (int)min((long long)kPrologueThreads, lo + cnt - base);
@@ -194,7 +233,9 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long
   __syncthreads();
   const int t = threadIdx.x;
   bool survive = false;
+  int lane_kind = -1;  // survivor routed to the lane tier (its kind)
   Pre pre;
+  LaneRec lr;
   if (t < nb) {
     const long long q = base + t;
     const double* P = tile + 24 * t;
@@ -233,23 +274,52 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long
           write_result(a, q, kHit, root, wb, 1, 0, 0);  // accepted at the root
         } else {
           survive = true;
-          for (int k = 0; k < 24; ++k) pre.P[k] = P[k];
-          pre.qp = qp;
-          pre.q = q;
-          pre.wb = wb;
-          pre.flag = make_flag(cls, acc, sdim, ph) | 64u;
-          pre.pad = 0;
+          int ex;
+          // lane tier: dyadic t_max (lattice boxes) and tame coordinates
+          if (lq && qp.tame && frexp(qp.t_max, &ex) == 0.5) {
+            lane_kind = qp.kind;
+            lr.q = q;
+            lr.wb = wb;
+            for (int k = 0; k < 3; ++k) { lr.eps[k] = qp.eps[k]; lr.kap[k] = qp.kap[k]; }
+            lr.sep = qp.sep;
+            lr.delta = qp.delta;
+            lr.t_max = qp.t_max;
+            lr.mc = qp.max_checks;
+          } else {
+            for (int k = 0; k < 24; ++k) pre.P[k] = P[k];
+            pre.qp = qp;
+            pre.q = q;
+            pre.wb = wb;
+#ifdef TCCD_DEBUG_ROOT_UNCLASSIFIED
+            pre.flag = 0;
+#else
+            pre.flag = make_flag(cls, acc, sdim, ph) | 64u;
+#endif
+            pre.pad = 0;
+          }
         }
       }
     }
   }
-  // warp-aggregated compaction
-  const unsigned int m = __ballot_sync(0xffffffffu, survive);
+  // warp-aggregated compaction: light-tier records, lane records per kind
+  // (vertex-face from the front of the lane queue, edge-edge from the back)
   const int lane = threadIdx.x & 31;
-  unsigned long long wbase = 0;
-  if (lane == 0 && m) wbase = atomicAdd(qcount, (unsigned long long)__popc(m));
-  wbase = __shfl_sync(0xffffffffu, wbase, 0);
-  if (survive) queue[wbase + __popc(m & ((1u << lane) - 1u))] = pre;
+  const unsigned int below = (1u << lane) - 1u;
+  const unsigned int m = __ballot_sync(0xffffffffu, survive && lane_kind < 0);
+  const unsigned int m0 = __ballot_sync(0xffffffffu, lane_kind == 0);
+  const unsigned int m1 = __ballot_sync(0xffffffffu, lane_kind == 1);
+  unsigned long long wb0 = 0, wb1 = 0, wb2 = 0;
+  if (lane == 0) {
+    if (m) wb0 = atomicAdd(qcount, (unsigned long long)__popc(m));
+    if (m0) wb1 = atomicAdd(&lcount[0], (unsigned long long)__popc(m0));
+    if (m1) wb2 = atomicAdd(&lcount[1], (unsigned long long)__popc(m1));
+  }
+  wb0 = __shfl_sync(0xffffffffu, wb0, 0);
+  wb1 = __shfl_sync(0xffffffffu, wb1, 0);
+  wb2 = __shfl_sync(0xffffffffu, wb2, 0);
+  if (survive && lane_kind < 0) queue[wb0 + __popc(m & below)] = pre;
+  if (lane_kind == 0) lq[wb1 + __popc(m0 & below)] = lr;
+  if (lane_kind == 1) lq[lq_cap - 1 - (long long)(wb2 + __popc(m1 & below))] = lr;
 }
 
 }  // namespace tccd
@@ -317,14 +387,32 @@ using GiantCfg = EngineCfg<TCCD_GNT, TCCD_GNT, 1, 0, 0, 0, false, TCCD_GMINB>;
 template <class Cfg>
 constexpr int groups_per_cta() { return Cfg::NT / Cfg::G; }
 
-__global__ void stats_kernel(Args a, int heavy_only) {
+__global__ void stats_kernel(Args a, int heavy_only, long long cnt) {
   if (threadIdx.x == 0 && a.stats) {
-    a.stats[0] += heavy_only ? (long long)a.ctr->q_count[2] : (long long)a.ctr->evicted[1];
-    a.stats[1] += (long long)a.ctr->rounds;
-    a.stats[2] += (long long)a.ctr->deferred;
-    a.stats[3] += (long long)a.ctr->evicted[0];
-    for (int k = 0; k < 3; ++k) a.stats[4 + k] += (long long)a.ctr->boxes[k];
-    for (int k = 0; k < 6; ++k) a.stats[8 + k] += (long long)a.ctr->cls[k / 2][k % 2];
+    const Counters& c = *a.ctr;
+    long long* S = a.stats;
+    S[TCCD_STAT_GIANT_QUERIES] += heavy_only ? (long long)c.q_count[2] : (long long)c.evicted[1];
+    S[TCCD_STAT_ROUNDS] += (long long)c.rounds;
+    S[TCCD_STAT_DEFERRALS] += (long long)c.deferred;
+    S[TCCD_STAT_MEDIUM_QUERIES] += (long long)c.evicted[0];
+    for (int k = 0; k < 3; ++k) S[TCCD_STAT_BOXES + k] += (long long)c.boxes[k];
+    S[TCCD_STAT_LANE_QUERIES] += (long long)(c.lane_count[0] + c.lane_count[1]);
+    for (int k = 0; k < 6; ++k) S[TCCD_STAT_CLS + k] += (long long)c.cls[k / 2][k % 2];
+    for (int k = 0; k < 2; ++k) {
+      S[TCCD_STAT_LANE_CLS + k] += (long long)c.lane[k];
+      S[TCCD_STAT_LANE_CHECKS + k] += (long long)c.lane[2 + k];
+      S[TCCD_STAT_LANE_DONE + k] += (long long)c.lane[4 + k];
+      S[TCCD_STAT_POOL_DEMAND + k] += (long long)c.pool[1 + k];
+      S[TCCD_STAT_RESTARTS + k] += (long long)c.restarts[k];
+    }
+    S[TCCD_STAT_LANE_EVICTED] += (long long)c.lane[6];
+    S[TCCD_STAT_LANE_WASTED] += (long long)c.lane[7];
+    for (int k = 0; k < 3; ++k) S[TCCD_STAT_TIER_CHECKS + k] += (long long)c.algo[k];
+    // survivors of the root check: the lane queue plus the prologue's light
+    // (heavy-only: giant) queue entries, which the lane tier's evictions joined
+    const unsigned long long into_light = heavy_only ? c.q_count[2] : c.q_count[0] - c.lane[6];
+    S[TCCD_STAT_PROLOGUE_DONE] += cnt - (long long)(c.lane_count[0] + c.lane_count[1] + into_light);
+    S[TCCD_STAT_CHUNKS] += 1;
   }
 }
 
@@ -333,6 +421,24 @@ __global__ void stats_kernel(Args a, int heavy_only) {
 __global__ void copy_out_kernel(const unsigned char* src, unsigned char* dst, long long bytes) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long stride = (long long)gridDim.x * blockDim.x;
+  const bool vec = (((uintptr_t)src | (uintptr_t)dst) & 15) == 0;
+  const long long n16 = vec ? bytes / 16 : 0;
+  for (long long i = t; i < n16; i += stride)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (long long i = n16 * 16 + t; i < bytes; i += stride) dst[i] = src[i];
+}
+
+// The same for the first min(*count, max_elems) elements of an array whose
+// length a kernel wrote (a compacted hit list): only those bytes cross.
+__global__ void copy_counted_kernel(const unsigned char* src, unsigned char* dst, long long elem,
+                                    const unsigned long long* count, long long max_elems,
+                                    unsigned long long* host_count) {
+  const unsigned long long c = *count;
+  const long long n = (long long)(c < (unsigned long long)max_elems ? c : (unsigned long long)max_elems);
+  const long long bytes = n * elem;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (t == 0 && host_count) *host_count = c;
   const bool vec = (((uintptr_t)src | (uintptr_t)dst) & 15) == 0;
   const long long n16 = vec ? bytes / 16 : 0;
   for (long long i = t; i < n16; i += stride)
@@ -381,32 +487,55 @@ using namespace tccd;
 
 namespace {
 
-constexpr long long kChunk = 1LL << 22;  // queries per host chunk
+#ifndef TCCD_CHUNK
+#define TCCD_CHUNK (1LL << 22)
+#endif
+#ifndef TCCD_POOL
+#define TCCD_POOL (1LL << 25)
+#endif
+constexpr long long kChunk = TCCD_CHUNK;       // queries per host chunk
+constexpr long long kPoolDefault = TCCD_POOL;  // handover pool boxes per tier transition
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  return dev;
+}
 
 int device_sm_count(int hint) {
   if (hint > 0) return hint;
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()) != cudaSuccess)
+    return 148;
   return sms > 0 ? sms : 148;
 }
 
 long long giant_cap(long long mcmax) { return 2 * mcmax + 2; }
 
-constexpr long long kPool = 1LL << 24;  // handover pool boxes per tier transition
-
 struct Layout {
-  size_t ctr, queue[3], hand[3], pbox[3], pflag[3], perm, light, medium, giant, total;
+  size_t ctr, queue[3], hand[3], pbox[3], pflag[3], perm, lq, lscratch, light, medium, giant, total;
   size_t light_b, medium_b, giant_b;
-  int light_blocks, medium_blocks, giant_blocks;
+  long long chunk, pool[3];
+  int light_blocks, medium_blocks, giant_blocks, lane_blocks;
 };
 
-Layout layout(long long n, long long mcmax, int giant_blocks, int sms) {
+// Everything scales with the chunk (min(n, kChunk) queries): queues, lane
+// scratch, one group per query at most in every tier, and handover pools no
+// larger than the chunk's largest possible handover (a query leaves the light
+// tier with at most 2 * LightCfg::QCAP boxes, the medium tier with at most
+// 2 * MediumCfg::QCAP).
+Layout layout(long long n, long long mcmax, int giant_blocks, int sms, long long pool_boxes) {
   Layout L;
   const long long chunk = n < kChunk ? (n > 0 ? n : 1) : kChunk;
-  L.light_blocks = TCCD_LMINB * sms;
-  L.medium_blocks = MediumCfg::MINB * sms;
-  L.giant_blocks = giant_blocks;
+  L.chunk = chunk;
+  const long long pool = pool_boxes > 0 ? pool_boxes : kPoolDefault;
+  L.pool[0] = 0;
+  L.pool[1] = std::min(pool, chunk * 2 * LightCfg::QCAP);
+  L.pool[2] = std::min(pool, chunk * 2 * MediumCfg::QCAP);
+  L.lane_blocks = (int)std::min<long long>((long long)TCCD_NMINB * sms, (chunk + kLaneNT - 1) / kLaneNT);
+  L.light_blocks = (int)std::min<long long>((long long)TCCD_LMINB * sms, chunk);
+  L.medium_blocks = (int)std::min<long long>((long long)MediumCfg::MINB * sms, chunk);
+  L.giant_blocks = (int)std::min<long long>(giant_blocks, chunk);
   L.light_b = align256(EngineArena<LightCfg>::bytes(LightCfg::CAP));
   L.medium_b = align256(EngineArena<MediumCfg>::bytes(MediumCfg::CAP));
   L.giant_b = align256(EngineArena<GiantCfg>::bytes(giant_cap(mcmax)));
@@ -416,10 +545,12 @@ Layout layout(long long n, long long mcmax, int giant_blocks, int sms) {
   L.hand[0] = L.pbox[0] = L.pflag[0] = 0;
   for (int k = 1; k < 3; ++k) {
     L.hand[k] = o; o += align256((size_t)chunk * sizeof(Hand));
-    L.pbox[k] = o; o += align256((size_t)kPool * sizeof(Box));
-    L.pflag[k] = o; o += align256((size_t)kPool);
+    L.pbox[k] = o; o += align256((size_t)L.pool[k] * sizeof(Box));
+    L.pflag[k] = o; o += align256((size_t)L.pool[k]);
   }
   L.perm = o; o += align256((size_t)kOrderMax * 4);
+  L.lq = o; o += align256((size_t)chunk * sizeof(LaneRec));
+  L.lscratch = o; o += align256((size_t)L.lane_blocks * kLaneNT * 3 * kLaneCap * 8);
   L.light = o; o += L.light_b * (size_t)L.light_blocks * groups_per_cta<LightCfg>();
   L.medium = o; o += L.medium_b * (size_t)L.medium_blocks * groups_per_cta<MediumCfg>();
   L.giant = o; o += L.giant_b * (size_t)L.giant_blocks;
@@ -427,15 +558,17 @@ Layout layout(long long n, long long mcmax, int giant_blocks, int sms) {
   return L;
 }
 
+// the dynamic shared-memory limit is a per-device attribute of the function
 template <class Cfg>
 int configure() {
-  static bool done = false;
-  if (done) return TCCD_OK;
+  static bool done[256] = {};
+  const int dev = current_device();
+  if (dev >= 0 && dev < 256 && done[dev]) return TCCD_OK;
   const int smem = (int)(engine_smem_bytes<Cfg>() * groups_per_cta<Cfg>());
   if (cudaFuncSetAttribute(engine_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            smem) != cudaSuccess)
     return TCCD_E_CUDA;
-  done = true;
+  if (dev >= 0 && dev < 256) done[dev] = true;
   return TCCD_OK;
 }
 
@@ -445,6 +578,14 @@ int launch_tier(const Args& a, const TierIO& io, int blocks, cudaStream_t st) {
   engine_kernel<Cfg><<<blocks, Cfg::NT, engine_smem_bytes<Cfg>() * groups_per_cta<Cfg>(), st>>>(a, io);
   return cudaGetLastError() == cudaSuccess ? TCCD_OK : TCCD_E_CUDA;
 }
+
+// tccd_solve_kernel's cached device scratch, per device
+struct ScratchCache {
+  unsigned char* buf = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_sk_mutex;
+ScratchCache g_sk[256];
 
 }  // namespace
 
@@ -468,6 +609,26 @@ int tccd_copy_to_host(const void* src, void* host_dst, int64_t bytes, void* stre
   return cudaGetLastError() == cudaSuccess ? TCCD_OK : TCCD_E_CUDA;
 }
 
+int tccd_copy_counted_to_host(const void* src, void* host_dst, int64_t elem_bytes,
+                              const uint64_t* count, int64_t max_elems, void* host_count,
+                              void* stream) {
+  if (elem_bytes <= 0 || max_elems < 0) return TCCD_E_N;
+  if (!src || !host_dst || !count) return TCCD_E_NULL;
+  void* dst = nullptr;
+  void* dcount = nullptr;
+  if (cudaHostGetDevicePointer(&dst, host_dst, 0) != cudaSuccess || !dst ||
+      (host_count && (cudaHostGetDevicePointer(&dcount, host_count, 0) != cudaSuccess || !dcount))) {
+    cudaGetLastError();
+    return TCCD_E_CUDA;
+  }
+  const long long n16 = (max_elems * elem_bytes) / 16;
+  const int blocks = (int)min(2LL * device_sm_count(0), max(1LL, (n16 + 255) / 256));
+  copy_counted_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      (const unsigned char*)src, (unsigned char*)dst, (long long)elem_bytes,
+      (const unsigned long long*)count, (long long)max_elems, (unsigned long long*)dcount);
+  return cudaGetLastError() == cudaSuccess ? TCCD_OK : TCCD_E_CUDA;
+}
+
 const char* tccd_error_string(int code) {
   switch (code) {
     case TCCD_OK: return "ok";
@@ -486,16 +647,24 @@ const char* tccd_error_string(int code) {
   }
 }
 
-size_t tccd_workspace_bytes(int64_t n, int64_t max_checks_max, int32_t heavy_blocks) {
-  if (n < 0 || max_checks_max < 1) return 0;
+size_t tccd_workspace_bytes_ex(int64_t n, int64_t max_checks_max, int32_t heavy_blocks,
+                               int64_t pool_boxes) {
+  if (n < 0 || max_checks_max < 1 || pool_boxes < 0) return 0;
   const int sms = device_sm_count(0);
   const int gb = heavy_blocks > 0 ? heavy_blocks : sms;
-  return layout(n, max_checks_max, gb, sms).total;
+  return layout(n, max_checks_max, gb, sms, pool_boxes).total;
 }
 
-int tccd_solve_batch(const tccd_batch* b, void* stream) {
-  if (!b) return TCCD_E_NULL;
-  if (b->struct_size != sizeof(tccd_batch)) return TCCD_E_STRUCT;
+size_t tccd_workspace_bytes(int64_t n, int64_t max_checks_max, int32_t heavy_blocks) {
+  return tccd_workspace_bytes_ex(n, max_checks_max, heavy_blocks, 0);
+}
+
+int tccd_solve_batch(const tccd_batch* b_in, void* stream) {
+  if (!b_in) return TCCD_E_NULL;
+  if (b_in->struct_size != sizeof(tccd_batch)) return TCCD_E_STRUCT;
+  tccd_batch* out_b = const_cast<tccd_batch*>(b_in);
+  out_b->launches = 0;
+  const tccd_batch* b = b_in;
   if (b->n < 0) return TCCD_E_N;
   if (b->n > 0 && (!b->points || !b->status || !b->toi)) return TCCD_E_NULL;
   if (!b->delta && !(b->delta_all > 0.0 && b->delta_all < 1.0 / 0.0)) return TCCD_E_DELTA;
@@ -507,12 +676,16 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
   const long long mcmax = b->max_checks ? b->max_checks_max : b->max_checks_all;
   if (b->max_checks && mcmax < 1) return TCCD_E_MAXCHECKS;
   if (giant_cap(mcmax) > (long long)kRefSrcMask) return TCCD_E_CAPACITY;
+  if (b->pool_boxes < 0) return TCCD_E_WORKSPACE;
+  if (b->hit_index && (!b->hit_toi || !b->hit_count || b->hit_capacity < 0)) return TCCD_E_NULL;
   const int sms = device_sm_count(b->device_sms);
   const int gb = b->heavy_blocks > 0 ? b->heavy_blocks : sms;
-  const Layout L = layout(b->n, mcmax, gb, sms);
+  const Layout L = layout(b->n, mcmax, gb, sms, b->pool_boxes);
   if (!b->workspace || b->workspace_bytes < L.total) return TCCD_E_WORKSPACE;
-  if (b->n == 0) return TCCD_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  if (b->stats && cudaMemsetAsync(b->stats, 0, TCCD_NUM_STATS * sizeof(int64_t), st) != cudaSuccess)
+    return TCCD_E_CUDA;
+  if (b->n == 0) return TCCD_OK;
   unsigned char* ws = (unsigned char*)b->workspace;
 
   Args a;
@@ -542,6 +715,13 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
   a.stats = (long long*)b->stats;
   a.ctr = (Counters*)(ws + L.ctr);
   a.heavy_only = (b->flags & TCCD_FLAG_HEAVY_ONLY) ? 1 : 0;
+  a.no_lane = (b->flags & TCCD_FLAG_NO_LANE) ? 1 : 0;
+  a.hit_index = (long long*)b->hit_index;
+  a.hit_toi = b->hit_toi;
+  a.hit_count = (unsigned long long*)b->hit_count;
+  a.hit_cap = b->hit_capacity;
+  a.hit_base = b->hit_index_base;
+  const bool lanes = !a.heavy_only && !a.no_lane;
 
   Pre* queue[3];
   for (int k = 0; k < 3; ++k) queue[k] = (Pre*)(ws + L.queue[k]);
@@ -559,7 +739,8 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
     io.out_pbox = tier < 2 ? (Box*)(ws + L.pbox[tier + 1]) : nullptr;
     io.out_pflag = tier < 2 ? (uint8_t*)(ws + L.pflag[tier + 1]) : nullptr;
     io.out_pool_count = tier < 2 ? &a.ctr->pool[tier + 1] : nullptr;
-    io.pool_cap = kPool;
+    io.pool_cap = tier < 2 ? L.pool[tier + 1] : 0;
+    io.in_pool_cap = L.pool[tier];
     io.in_count = &a.ctr->q_count[tier];
     io.in_next = &a.ctr->q_next[tier];
     io.out = tier < 2 ? queue[tier + 1] : nullptr;
@@ -570,18 +751,28 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
     io.boxes = &a.ctr->boxes[tier];
     io.phase = a.ctr->phase[tier];
     io.cls = a.ctr->cls[tier];
+    io.restarts = &a.ctr->restarts[tier];
+    io.algo = &a.ctr->algo[tier];
     if (tier == 0) { io.arenas = ws + L.light; io.arena_bytes = L.light_b; io.cap = LightCfg::CAP; }
     if (tier == 1) { io.arenas = ws + L.medium; io.arena_bytes = L.medium_b; io.cap = MediumCfg::CAP; }
     if (tier == 2) { io.arenas = ws + L.giant; io.arena_bytes = L.giant_b; io.cap = giant_cap(mcmax); }
     return io;
   };
+  LaneIO lio;
+  lio.rec = (const LaneRec*)(ws + L.lq);
+  lio.rec_cap = L.chunk;
+  lio.count = a.ctr->lane_count;
+  lio.next = a.ctr->lane_next;
+  lio.scratch = (unsigned long long*)(ws + L.lscratch);
+  lio.out = queue[0];
+  lio.out_count = &a.ctr->q_count[0];
+  lio.stats = a.ctr->lane;
 
   // optional caller events, recorded after each stage of every chunk
   auto mark = [&](int k) {
     return b->events && b->events[k] ? cudaEventRecord((cudaEvent_t)b->events[k], st) : cudaSuccess;
   };
-  if (a.stats && cudaMemsetAsync(a.stats, 0, 16 * sizeof(long long), st) != cudaSuccess)
-    return TCCD_E_CUDA;
+  long long launches = 0;
   for (long long lo = 0; lo < b->n; lo += kChunk) {
     const long long cnt = b->n - lo < kChunk ? b->n - lo : kChunk;
     if (cudaMemsetAsync(a.ctr, 0, sizeof(Counters), st) != cudaSuccess) return TCCD_E_CUDA;
@@ -591,30 +782,45 @@ int tccd_solve_batch(const tccd_batch* b, void* stream) {
 #endif
     const int first = a.heavy_only ? 2 : 0;
     const unsigned pblocks = (unsigned)((cnt + kPrologueThreads - 1) / kPrologueThreads);
-    prologue_kernel<<<pblocks, kPrologueThreads, 0, st>>>(a, lo, cnt, queue[first],
-                                                         &a.ctr->q_count[first]);
-    if (cudaGetLastError() != cudaSuccess || mark(0) != cudaSuccess) return TCCD_E_CUDA;
+    prologue_kernel<<<pblocks, kPrologueThreads, 0, st>>>(
+        a, lo, cnt, queue[first], &a.ctr->q_count[first],
+        lanes ? (LaneRec*)(ws + L.lq) : nullptr, L.chunk, a.ctr->lane_count);
+    ++launches;
+    if (cudaGetLastError() != cudaSuccess || mark(TCCD_STAGE_PROLOGUE) != cudaSuccess)
+      return TCCD_E_CUDA;
+    if (lanes) {
+      lane_kernel<<<L.lane_blocks, kLaneNT, 0, st>>>(a, lio);
+      ++launches;
+      if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
+    }
+    if (mark(TCCD_STAGE_LANE) != cudaSuccess) return TCCD_E_CUDA;
     int rc;
     if (!a.heavy_only) {
       if ((rc = launch_tier<LightCfg>(a, io_for(0), L.light_blocks, st)) != TCCD_OK) return rc;
-      if (mark(1) != cudaSuccess) return TCCD_E_CUDA;
+      ++launches;
+      if (mark(TCCD_STAGE_LIGHT) != cudaSuccess) return TCCD_E_CUDA;
       if ((rc = launch_tier<MediumCfg>(a, io_for(1), L.medium_blocks, st)) != TCCD_OK) return rc;
-      if (mark(2) != cudaSuccess) return TCCD_E_CUDA;
-    } else if (mark(1) != cudaSuccess || mark(2) != cudaSuccess) {
+      ++launches;
+      if (mark(TCCD_STAGE_MEDIUM) != cudaSuccess) return TCCD_E_CUDA;
+    } else if (mark(TCCD_STAGE_LIGHT) != cudaSuccess || mark(TCCD_STAGE_MEDIUM) != cudaSuccess) {
       return TCCD_E_CUDA;
     }
     if (!a.heavy_only) {
       order_kernel<<<1, 1024, 0, st>>>((const Hand*)(ws + L.hand[2]), &a.ctr->q_count[2],
                                        (unsigned int*)(ws + L.perm));
+      ++launches;
       if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
     }
     if ((rc = launch_tier<GiantCfg>(a, io_for(2), L.giant_blocks, st)) != TCCD_OK) return rc;
-    if (mark(3) != cudaSuccess) return TCCD_E_CUDA;
+    ++launches;
+    if (mark(TCCD_STAGE_GIANT) != cudaSuccess) return TCCD_E_CUDA;
     if (a.stats) {
-      stats_kernel<<<1, 32, 0, st>>>(a, a.heavy_only);
+      stats_kernel<<<1, 32, 0, st>>>(a, a.heavy_only, cnt);
+      ++launches;
       if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
     }
   }
+  out_b->launches = launches;
   return TCCD_OK;
 }
 
@@ -630,9 +836,21 @@ int tccd_solve_kernel(const double* s, const double* e, int kind, double t_max, 
   const int gb = 1;
   const size_t ws_bytes = tccd_workspace_bytes(1, max_checks, gb);
   const size_t in_b = 256, out_b = 256;  // inputs | outputs | workspace
-  unsigned char* d = nullptr;
-  if (cudaMalloc(&d, in_b + out_b + ws_bytes) != cudaSuccess) return TCCD_E_CUDA;
-  int rc = TCCD_OK;
+  std::lock_guard<std::mutex> lock(g_sk_mutex);
+  const int dev = current_device();
+  if (dev < 0 || dev >= 256) return TCCD_E_CUDA;
+  ScratchCache& sc = g_sk[dev];
+  if (sc.bytes < in_b + out_b + ws_bytes) {
+    if (sc.buf) cudaFree(sc.buf);
+    sc.buf = nullptr;
+    sc.bytes = 0;
+    if (cudaMalloc(&sc.buf, in_b + out_b + ws_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return TCCD_E_CUDA;
+    }
+    sc.bytes = in_b + out_b + ws_bytes;
+  }
+  unsigned char* d = sc.buf;
   double* d_pts = (double*)d;
   double* d_eps = d_pts + 24;
   unsigned char* o = d + in_b;
@@ -644,11 +862,11 @@ int tccd_solve_kernel(const double* s, const double* e, int kind, double t_max, 
   int* d_level = (int*)(d_toi + 10);
   uint8_t* d_status = (uint8_t*)(d_toi + 11);
   uint8_t* d_early = d_status + 1;
+  // (a private non-blocking stream would need its own synchronization: the
+  // legacy stream orders these copies with the solve)
   if (cudaMemcpy(d_pts, hpts, sizeof hpts, cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(d_eps, heps, sizeof heps, cudaMemcpyHostToDevice) != cudaSuccess) {
-    cudaFree(d);
+      cudaMemcpy(d_eps, heps, sizeof heps, cudaMemcpyHostToDevice) != cudaSuccess)
     return TCCD_E_CUDA;
-  }
   tccd_batch b;
   memset(&b, 0, sizeof b);
   b.struct_size = sizeof b;
@@ -672,11 +890,10 @@ int tccd_solve_kernel(const double* s, const double* e, int kind, double t_max, 
   b.workspace = o + out_b;
   b.workspace_bytes = ws_bytes;
   b.heavy_blocks = gb;
-  rc = tccd_solve_batch(&b, nullptr);
+  int rc = tccd_solve_batch(&b, nullptr);
   unsigned char host[out_b];
   if (rc == TCCD_OK && cudaMemcpy(host, o, out_b, cudaMemcpyDeviceToHost) != cudaSuccess)
     rc = TCCD_E_CUDA;
-  cudaFree(d);
   if (rc != TCCD_OK) return rc;
   const double* hd = (const double*)host;
   long long chk;
@@ -693,6 +910,19 @@ int tccd_solve_kernel(const double* s, const double* e, int kind, double t_max, 
   for (int k = 0; k < 6; ++k) out13[6 + k] = hd[3 + k];
   out13[12] = lvl;
   return TCCD_OK;
+}
+
+void tccd_release_cached(void) {
+  std::lock_guard<std::mutex> lock(g_sk_mutex);
+  int cur = current_device();
+  for (int d = 0; d < 256; ++d) {
+    if (!g_sk[d].buf) continue;
+    cudaSetDevice(d);
+    cudaFree(g_sk[d].buf);
+    g_sk[d].buf = nullptr;
+    g_sk[d].bytes = 0;
+  }
+  cudaSetDevice(cur);
 }
 
 }  // extern "C"

@@ -320,6 +320,7 @@ struct EngineShared {
   QueryParams qp[Q];
   Rec rec[Q][2];         // [0] first, [1] drop
   long long C[Q];        // checks before the current level
+  long long C0[Q];       // checks when the query entered this tier
   long long qidx[Q];     // -1: free slot
   double root_wb[Q];
   int level[Q];
@@ -420,6 +421,7 @@ struct TierIO {
   long long pool_cap;
   unsigned long long* in_count;
   unsigned long long* in_next;
+  long long in_pool_cap;    // boxes in the input handover pool
   Pre* out;                 // eviction queue of the next tier (nullptr: none)
   unsigned long long* out_count;
   unsigned char* arenas;
@@ -431,6 +433,8 @@ struct TierIO {
   unsigned long long* boxes;
   unsigned long long* phase;  // [16] cycles per phase (TCCD_PHASE_PROF builds)
   unsigned long long* cls;    // [2] box classifications (VF, EE)
+  unsigned long long* restarts;  // evictions that found the handover pool full
+  unsigned long long* algo;      // checks of the reference's path done here
 };
 
 template <class Cfg>
@@ -479,6 +483,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   bool cprv = false;  // the previous round's level arrays are compact
   long long rounds = 0;
   unsigned long long evicted = 0, boxes = 0;
+  long long algo = 0;  // this thread's share of the tier's algorithmic checks
   unsigned int ncls_vf = 0, ncls_ee = 0;  // this thread's classifications per kind
 #ifdef TCCD_PHASE_PROF
   unsigned long long ph_acc[16] = {0};
@@ -502,6 +507,11 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
     if (io.out_hand) {
       const unsigned long long o = atomicAdd(io.out_pool_count, (unsigned long long)t);
       if ((long long)o + t <= io.pool_cap) off = (long long)o;
+      if (off < 0) {
+        // restart from the root: this tier's checks of the query are redone
+        atomicAdd(io.restarts, 1ull);
+        algo -= S.C[s] - S.C0[s];
+      }
       Hand& hd = io.out_hand[h];
       hd.n = off >= 0 ? t : 0;
       hd.off = off;
@@ -626,6 +636,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           S.w[s][0] = pb.t1 - pb.t0; S.w[s][1] = pb.u1 - pb.u0; S.w[s][2] = pb.v1 - pb.v0;
         }
         S.C[s] = hd.C;
+        S.C0[s] = hd.C;
         S.level[s] = hd.level;
         S.rec[s][0] = hd.rec[0];
         S.rec[s][1] = hd.rec[1];
@@ -633,6 +644,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         S.have_drop[s] = hd.have_drop;
       } else {
         S.C[s] = 0;
+        S.C0[s] = 0;
         S.level[s] = 0;
         S.have_first[s] = 0;
         S.have_drop[s] = 0;
@@ -666,13 +678,14 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         }
       } else {
         for (int b = tid; b < nr; b += NT) {
-          TCCD_ASSERT(pos + b < cap && off + b < io.pool_cap);
+          TCCD_ASSERT(pos + b < cap && off + b < io.in_pool_cap);
           pick(ar.ref, cur)[pos + b] = kRefExt | (unsigned)(off + b);
           pick(slot_of, cur)[pos + b] = (uint8_t)s;
           pick(flags, cur)[pos + b] = io.in_pflag[off + b];
         }
       }
     }
+    gsync<G>();  // (seg_off, written by thread 0 above, sets every slot's budget cut below)
     }  // k_adm > 0
     for (int s = tid; s < Q; s += NT) {
       S.hoff[s] = -1;
@@ -808,6 +821,13 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
           if (up) b.v0 = mid; else b.v1 = mid;
         }
       }
+#ifdef TCCD_DEBUG_ROOT
+      if ((r & kRefRoot) && (r & kRefExt) != kRefExt) {
+        if (f & kClassified) atomicAdd(&io.phase[13], 1ull);
+        else if (!(i <= S.cutpos[s])) atomicAdd(&io.phase[14], 1ull);
+        else atomicAdd(&io.phase[15], 1ull);
+      }
+#endif
       if (!(f & kClassified)) {
         if (i <= S.cutpos[s]) {
           const uint8_t head = f & kHead;
@@ -872,14 +892,28 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       const long long ecls = nn < cut + 1 ? nn : cut + 1;
       const int j = S.j[s] == kIntMax ? kIntMax : S.j[s] - S.seg_off[s];  // (segment-relative)
       bool done = true;
+#ifdef TCCD_DEBUG_ROOT
+      if (j >= ecls && S.level[s] == 0 && C == 0 && !(S.root_flag[s] & kClassified)) {
+        const Box rb = {0.0, S.qp[s].t_max, 0.0, 1.0, 0.0, 1.0};
+        double w2;
+        const int c2 = classify((const double*)S.P[s], S.qp[s].kind, rb, S.qp[s].eps, S.qp[s].sep, w2,
+                                S.qp[s].tame != 0);
+        if (c2 != kDisjoint) atomicAdd(&io.phase[12], 1ull);
+        if (c2 != kDisjoint && nn != 1) atomicAdd(&io.phase[11], 1ull);
+        if (c2 != kDisjoint) atomicAdd(&io.phase[10], (unsigned long long)(fl[S.seg_off[s]]));
+      }
+#endif
       if (j >= ecls) {
         if (cut < nn) {
+          algo += mc - C;
           if (S.have_drop[s] || cut + 1 < nn) finish(s, true, mc);
           else free_result(s, mc);
         } else if (S.have_drop[s]) {
+          algo += nn;
           const Rec& r = S.rec[s][1];
           write_result(a, S.qidx[s], kHit, r.b, r.codom, C + nn, 0, r.level);
         } else {
+          algo += nn;
           free_result(s, C + nn);
         }
       } else {
@@ -892,8 +926,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         fr.level = S.level[s];
         S.have_first[s] = 1;
         if (j == cut) {
+          algo += mc - C;
           finish(s, true, mc);
         } else if (fl[ij] & 4) {
+          algo += j + 1;
           // first colliding box of a fresh level accepted (_kernel.py:243-252)
           if (S.have_drop[s] && S.rec[s][1].b.t0 < bj.t0) {
             const Rec& r = S.rec[s][1];
@@ -915,8 +951,10 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
             S.have_drop[s] = 1;
           }
           if (cut < nn) {
+            algo += mc - C;
             finish(s, true, mc);
           } else {
+            algo += nn;
             done = false;
             S.cont[s] = 1;
             S.C[s] = C + nn;
@@ -1466,6 +1504,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
         }
       } else if (S.cont[s] == 2) {
         S.C[s] -= S.seg_n[s];  // the level re-runs next round
+        algo -= S.seg_n[s];
         S.seg_off[s] = S.next_off[s];
       }
     }
@@ -1492,6 +1531,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
 #endif
   }
   if (evicted) atomicAdd(io.evicted, evicted);
+  if (algo) atomicAdd(io.algo, (unsigned long long)algo);  // (two's complement: a signed sum)
   {  // (all lanes reach here: the round loop exits group-wide)
     const unsigned int wv = __reduce_add_sync(0xffffffffu, ncls_vf);
     const unsigned int we = __reduce_add_sync(0xffffffffu, ncls_ee);

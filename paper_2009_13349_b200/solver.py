@@ -21,8 +21,10 @@ from .core import CCDResult, DomainBox, Query, QueryKind, SolverConfig
 from .inclusion import FilterEps
 
 OUTPUT_FIELDS = ("status", "toi", "tol", "codom", "checks", "early", "witness", "level")
+STAGES = _lib.STAGES
 
 _workspaces: dict = {}
+_ws_last: dict = {}  # device -> (stream handle, event) of the last call that used the workspace
 _copy_streams: dict = {}
 _staging: dict = {}  # device -> list of [uint8 tensor, torch.cuda.Event | None]
 
@@ -66,6 +68,7 @@ def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
     key = (device.type, device.index)
     ws = _workspaces.get(key)
     if ws is None or ws.numel() < nbytes:
+        _ws_last.pop(device.index, None)  # (the synchronize below orders every user)
         # drop the smaller cached workspace (and give its memory back) before
         # allocating the larger one: both would not fit at ~100 GB sizes
         _workspaces.pop(key, None)
@@ -78,8 +81,25 @@ def _workspace(device: torch.device, nbytes: int) -> torch.Tensor:
     return ws
 
 
+def _workspace_guard(device: torch.device, stream: torch.cuda.Stream) -> None:
+    """The device's cached workspace (counters, queues, pools, arenas) is
+    shared by every call on that device (solve_batch, irf_batch): a call on
+    another stream than the previous one waits for that call's work first,
+    so calls on different streams never run on the same memory at once."""
+    last = _ws_last.get(device.index)
+    if last is not None and last[0] != stream.cuda_stream:
+        stream.wait_event(last[1])
+
+
+def _workspace_release(device: torch.device, stream: torch.cuda.Stream) -> None:
+    ev = torch.cuda.Event()
+    ev.record(stream)
+    _ws_last[device.index] = (stream.cuda_stream, ev)
+
+
 def release_workspaces() -> None:
     _workspaces.clear()
+    _ws_last.clear()
     _heavy_blocks_cache.clear()
 
 
@@ -124,8 +144,9 @@ def _default_heavy_blocks(device: torch.device, n: int, max_checks_max: int) -> 
     return max(1, min(sms, max(int(n), 1), int(budget // per)))
 
 
-def workspace_bytes(n: int, max_checks_max: int, heavy_blocks: int) -> int:
-    return int(_lib.lib().tccd_workspace_bytes(int(n), int(max_checks_max), int(heavy_blocks)))
+def workspace_bytes(n: int, max_checks_max: int, heavy_blocks: int, pool_boxes: int = 0) -> int:
+    return int(_lib.lib().tccd_workspace_bytes_ex(int(n), int(max_checks_max), int(heavy_blocks),
+                                                  int(pool_boxes)))
 
 
 def _param(x, n, dtype, device, name):
@@ -170,7 +191,9 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
                 max_checks=None, separation=None, t_max=None, eps=None,
                 outputs=OUTPUT_FIELDS, device=None, heavy_only: bool = False,
                 heavy_blocks: int | None = None, raise_on_error: bool = True,
-                stats: bool = False, events=None, non_blocking: bool = False) -> dict:
+                stats: bool = False, events=None, non_blocking: bool = False,
+                hits: bool = False, lanes: bool = True, pool_boxes: int = 0,
+                info: dict | None = None, poison: bool = False) -> dict:
     """Solve a batch of CCD queries on one GPU.
 
     points: [n, 8, 3] float64 (torch tensor or numpy), start block then end
@@ -193,10 +216,23 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
     the launching stream) has completed, and per-query errors are not
     raised (check status after synchronizing).
 
-    stats=True adds out["stats"], the library's 16 diagnostic counters
-    (include/tccd.h).  events: optional 4 torch.cuda.Event(enable_timing=True),
-    recorded on the launching stream after the prologue, light, medium and
-    giant stages (per-kernel timing).
+    stats=True adds out["stats"], the library's diagnostic counters
+    (TCCD_STAT_*, include/tccd.h).  events: optional len(STAGES)
+    torch.cuda.Event(enable_timing=True), recorded on the launching stream
+    after the prologue, lane, light, medium and giant stages (per-kernel
+    timing).  info: an optional dict that receives "launches", the number of
+    kernels the call launched.
+
+    hits=True adds the compacted hit list: out["hit_index"] (int64) and
+    out["hit_toi"] (float64), one entry per query with status 1 in no
+    particular order, and out["hit_count"].  With device inputs the arrays
+    have capacity n and hit_count is a device tensor ([1], the entry
+    count); with host inputs only the live entries are copied back (and
+    with non_blocking=True, by a kernel reading the device count: no host
+    synchronization; trim with hit_count after out["ready"]).
+
+    lanes=False routes every query through the group tiers (diagnostics);
+    pool_boxes sets the handover pool size (0: library default).
     """
     config = config or SolverConfig()
     host_in = not (isinstance(points, torch.Tensor) and points.is_cuda)
@@ -280,21 +316,35 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
     if "early" in want: out["early"] = torch.empty(n, dtype=torch.uint8, device=dev)
     if "witness" in want: out["witness"] = torch.empty((n, 6), dtype=torch.float64, device=dev)
     if "level" in want: out["level"] = torch.empty(n, dtype=torch.int32, device=dev)
-    st = torch.zeros(16, dtype=torch.int64, device=dev) if stats else None
+    if poison:
+        # diagnostics: every output starts as a sentinel (status 0xEE, NaN
+        # payloads), so a query whose result is never written shows up
+        out["status"].fill_(0xEE)
+        for k, v in out.items():
+            if k != "status":
+                v.view(torch.uint8).fill_(0xEE)
+    if hits:
+        out["hit_index"] = torch.empty(n, dtype=torch.int64, device=dev)
+        out["hit_toi"] = torch.empty(n, dtype=torch.float64, device=dev)
+        out["hit_count"] = torch.zeros(1, dtype=torch.int64, device=dev)
+    st = torch.zeros(_lib.NUM_STATS, dtype=torch.int64, device=dev) if stats else None
     ev_arr = None
     if events is not None:
-        if len(events) != 4:
-            raise ValueError("events must hold 4 torch.cuda.Event")
+        if len(events) != len(STAGES):
+            raise ValueError(f"events must hold {len(STAGES)} torch.cuda.Event")
         for ev in events:
             if ev.cuda_event == 0:  # torch creates the handle on first record
                 ev.record(torch.cuda.current_stream(dev))
-        ev_arr = (ctypes.c_void_p * 4)(*[ev.cuda_event for ev in events])
+        ev_arr = (ctypes.c_void_p * len(STAGES))(*[ev.cuda_event for ev in events])
+    flags = (_lib.FLAG_HEAVY_ONLY if heavy_only else 0) | (0 if lanes else _lib.FLAG_NO_LANE)
+    n_launch = [0]
 
     with torch.cuda.device(dev):
         hb = heavy_blocks or default_heavy_blocks(dev, n, mc_max)
-        nbytes = workspace_bytes(n, mc_max, hb)
+        nbytes = workspace_bytes(n, mc_max, hb, pool_boxes)
         ws = _workspace(dev, nbytes)
         stream = torch.cuda.current_stream(dev)
+        _workspace_guard(dev, stream)
 
         def sl(t, lo, hi):
             return None if t is None else t[lo:hi]
@@ -302,7 +352,7 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
         def launch(lo, hi, ev_arr=None):
             b = _lib.TccdBatch()
             b.struct_size = ctypes.sizeof(_lib.TccdBatch)
-            b.flags = _lib.FLAG_HEAVY_ONLY if heavy_only else 0
+            b.flags = flags
             b.n = hi - lo
             b.points = _ptr(pts[lo:hi])
             b.kind = _ptr(sl(kind_t, lo, hi))
@@ -325,7 +375,15 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
             b.device_sms = sm_count(dev)
             b.stats = _ptr(st)
             b.events = ctypes.cast(ev_arr, ctypes.c_void_p) if ev_arr is not None else None
+            if hits:
+                b.hit_index = _ptr(out["hit_index"])
+                b.hit_toi = _ptr(out["hit_toi"])
+                b.hit_count = _ptr(out["hit_count"])
+                b.hit_capacity = n
+                b.hit_index_base = lo
+            b.pool_boxes = int(pool_boxes)
             rc = lib.tccd_solve_batch(ctypes.byref(b), ctypes.c_void_p(stream.cuda_stream))
+            n_launch[0] += int(b.launches)
             _raise_abi(rc, delta_all, mc_all, tm_all, sep_all, kind_all)
 
         if chunk_events is None:
@@ -334,6 +392,7 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
             for c, ev in enumerate(chunk_events):
                 stream.wait_event(ev)
                 launch(c * CHUNK, min(n, (c + 1) * CHUNK))
+        _workspace_release(dev, stream)
     if host_in and non_blocking:
         # results into pinned host tensors by a copy kernel on the launching
         # stream, not the copy engines: engine copies are served in submission
@@ -342,14 +401,44 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
         stream = torch.cuda.current_stream(dev)
         hout = {}
         for k, v in out.items():
+            if k in ("hit_index", "hit_toi", "hit_count"):
+                continue
+            if hits and k not in outputs:
+                continue  # (with a hit list only the named dense fields come back)
             h = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-            if v.numel() and lib.tccd_copy_to_host(_ptr(v), _ptr(h), v.numel() * v.element_size(),
-                                                   ctypes.c_void_p(stream.cuda_stream)) != 0:
-                h.copy_(v, non_blocking=True)  # (not device-accessible: an engine copy)
+            if v.numel():
+                if lib.tccd_copy_to_host(_ptr(v), _ptr(h), v.numel() * v.element_size(),
+                                         ctypes.c_void_p(stream.cuda_stream)) != 0:
+                    h.copy_(v, non_blocking=True)  # (not device-accessible: an engine copy)
+                else:
+                    n_launch[0] += 1
             hout[k] = h
+        if hits:
+            # only the live entries of the hit list cross (the kernels read the
+            # device count); trim with hit_count once out["ready"] completed
+            hc = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+            for k in ("hit_index", "hit_toi"):
+                v = out[k]
+                h = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                if n:
+                    _lib.check(lib.tccd_copy_counted_to_host(
+                        _ptr(v), _ptr(h), 8, _ptr(out["hit_count"]), n,
+                        _ptr(hc) if k == "hit_index" else None,
+                        ctypes.c_void_p(stream.cuda_stream)), "tccd_copy_counted_to_host")
+                    n_launch[0] += 1
+                hout[k] = h
+            hout["hit_count"] = hc
         out = hout
     elif host_in:
-        out = {k: v.to("cpu", non_blocking=True) for k, v in out.items()}
+        if hits and "status" not in outputs and raise_on_error and n:
+            _raise_status(out["status"])  # (on the device: the dense status stays there)
+        if hits:
+            # only the live entries cross: the count first (one small sync)
+            cnt = int(out["hit_count"].item())
+            out["hit_index"] = out["hit_index"][:cnt]
+            out["hit_toi"] = out["hit_toi"][:cnt]
+        out = {k: v.to("cpu", non_blocking=True) for k, v in out.items()
+               if not hits or k in outputs or k.startswith("hit_")}
     if host_in:
         if non_blocking:
             ready = torch.cuda.Event()
@@ -359,11 +448,15 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
                 slot[1] = ready  # the staging buffer is free once this solve is done
             if st is not None:
                 out["stats"] = st
+            if info is not None:
+                info["launches"] = n_launch[0]
             return out
         torch.cuda.current_stream(dev).synchronize()
     if st is not None:
         out["stats"] = st
-    if raise_on_error and n:
+    if info is not None:
+        info["launches"] = n_launch[0]
+    if raise_on_error and n and "status" in out:
         _raise_status(out["status"])
     return out
 

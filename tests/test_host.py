@@ -184,7 +184,7 @@ def test_library_exports_every_header_symbol():
     assert set(syms) == set(_lib.EXPORTS)
     for name in syms:
         assert hasattr(L, name), name
-    assert L.tccd_abi_version() == _lib.ABI_VERSION == 2
+    assert L.tccd_abi_version() == _lib.ABI_VERSION == 3
     for code in range(0, 12):
         assert L.tccd_error_string(code)
     assert b"unknown" in L.tccd_error_string(999)
@@ -219,6 +219,24 @@ def test_workspace_bytes_is_monotone_and_rejects_bad_sizes():
     assert 0 < a < b < c
     assert L.tccd_workspace_bytes(-1, 10, 1) == 0
     assert L.tccd_workspace_bytes(10, 0, 1) == 0
+    assert L.tccd_workspace_bytes_ex(10, 10, 1, -1) == 0
+
+
+def test_workspace_scales_with_the_batch():
+    """Queues, lane scratch, group arenas and handover pools follow the batch
+    size: one query at m_I = 1e6 needs its giant arena (2 m_I + 2 boxes) and
+    little else, so the per-call drop-in is not a multi-GB allocation."""
+    from paper_2009_13349_b200 import _lib
+    L = _lib.lib()
+    one = L.tccd_workspace_bytes(1, 1_000_000, 1)
+    assert one < 400e6
+    small = L.tccd_workspace_bytes(1, 1000, 1)
+    assert small < 20e6
+    sizes = [L.tccd_workspace_bytes(n, 1000, 1) for n in (1, 10, 1000, 100_000, 1 << 22, 1 << 23)]
+    assert all(a <= b for a, b in zip(sizes, sizes[1:]))
+    assert sizes[-1] == sizes[-2]  # bounded by one library chunk
+    # the handover pool size is a parameter; a smaller pool never grows the layout
+    assert L.tccd_workspace_bytes_ex(1 << 20, 1000, 1, 1 << 16) < L.tccd_workspace_bytes(1 << 20, 1000, 1)
 
 
 def test_solve_batch_fails_loudly_without_gpu():
