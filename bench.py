@@ -455,23 +455,15 @@ def main():
     if n * 192 <= 126e6:
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    # the library solves a batch in chunks and records its stage events once
-    # per chunk; a multi-chunk step is issued chunk by chunk here (the same
-    # kernels on the same stream) so that every chunk's stages are timed
-    CH = solver.CHUNK
-    nch = max(1, (n + CH - 1) // CH)
+    # the library records an event after every stage launch (prologue, lane,
+    # then light / medium / giant per group-tier sub-chunk); stage times are
+    # the gaps between consecutive events, summed per stage
+    NEV = 256
     NS = len(solver.STAGES)
 
     def step(events=None, info=None):
-        for j in range(nch):
-            a, b = j * CH, min(n, (j + 1) * CH)
-            kj = {k: v[a:b] for k, v in kw.items()}
-            inf = {}
-            solve_batch(pts[a:b], kind[a:b], outputs=("status", "toi"), device=dev,
-                        separation=sep, raise_on_error=False, info=inf,
-                        events=events[NS * j:NS * j + NS] if events else None, **kj)
-            if info is not None:
-                info["launches"] = info.get("launches", 0) + inf["launches"]
+        solve_batch(pts, kind, outputs=("status", "toi"), device=dev, separation=sep,
+                    raise_on_error=False, info=info, events=events, **kw)
 
     # untimed: full outputs once, for the algorithmic work (checks), hits and
     # the library's per-stage counters
@@ -495,21 +487,19 @@ def main():
     barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # per step: step start + the library's stage events per chunk, all on the
+    # per step: a start event + the library's stage events, all on the
     # launching stream; handles created here
-    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(1 + NS * nch)]
-           for _ in range(args.steps)]
+    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(1 + NEV)] for _ in range(args.steps)]
     for row in sev:
         for ev in row:
             ev.record(stream)
     torch.cuda.synchronize(dev)
-    launches = {}
-    step_ms = []
+    infos = [{} for _ in range(args.steps)]
     if flush is None:
         e0.record(stream)
         for k in range(args.steps):
             sev[k][0].record(stream)
-            step(sev[k][1:], launches)
+            step(sev[k][1:], infos[k])
         e1.record(stream)
         torch.cuda.synchronize(dev)
         ms = e0.elapsed_time(e1) / args.steps
@@ -517,15 +507,16 @@ def main():
         for k in range(args.steps):
             flush.fill_(k & 255)
             sev[k][0].record(stream)
-            step(sev[k][1:], launches)
+            step(sev[k][1:], infos[k])
         torch.cuda.synchronize(dev)
-        ms = statistics.mean(sev[k][0].elapsed_time(sev[k][-1]) for k in range(args.steps))
+        ms = statistics.mean(sev[k][0].elapsed_time(sev[k][len(infos[k]["event_stages"])])
+                             for k in range(args.steps))
     barrier()
-    # stage j of chunk c runs from event NS*c + j to NS*c + j + 1 (event 0: step start)
-    stage_ms = {nm: statistics.mean(sum(sev[k][NS * c + j].elapsed_time(sev[k][NS * c + j + 1])
-                                        for c in range(nch)) for k in range(args.steps))
-                for j, nm in enumerate(solver.STAGES)}
-    gpu_launches = launches.get("launches", 0)
+    per = [solver.stage_times(sev[k][0], sev[k][1:], infos[k]["event_stages"])
+           for k in range(args.steps)]
+    stage_ms = {nm: statistics.mean(p[nm] for p in per) for nm in solver.STAGES}
+    stage_launches = {nm: infos[0]["event_stages"].count(j) for j, nm in enumerate(solver.STAGES)}
+    gpu_launches = sum(i["launches"] for i in infos)
 
     # end to end through the public API with pinned host buffers
     e2e = None
@@ -633,9 +624,9 @@ def main():
                      "unit": "TFLOP/s", "frac": achieved / peaks["dfma_tflops"],
                      "traffic": traffic,
                      "kernel": KERNEL_NAMES[dom],
-                     "kernel_flops_per_launch": dom_flops / max(nch, 1),
-                     "kernel_ms_per_launch": stage_ms[dom] / max(nch, 1),
-                     "launches_per_step": nch,
+                     "kernel_flops_per_launch": dom_flops / max(stage_launches[dom], 1),
+                     "kernel_ms_per_launch": stage_ms[dom] / max(stage_launches[dom], 1),
+                     "launches_per_step": stage_launches[dom],
                      "share_of_step": stage_ms[dom] / ms,
                      "stages": per_stage,
                      "peak_source": "measured on this box: DFMA probe (libtccd_probe.so), "

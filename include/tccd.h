@@ -161,10 +161,25 @@ typedef struct tccd_batch {
   int32_t device_sms;   /* SM count of the target device; 0 = query it      */
   int64_t *stats;       /* optional device [TCCD_NUM_STATS] diagnostics
                            (TCCD_STAT_*)                                  */
-  void *const *events;  /* optional host array of TCCD_NUM_STAGES
-                           cudaEvent_t (NULL entries skipped), recorded on
-                           `stream` after each stage of each chunk:
-                           per-kernel timing on the launching stream     */
+  /* Per-kernel timing on the launching stream (ABI 3): events is an
+   * optional host array of n_events cudaEvent_t; the call records one after
+   * each stage it launches, in launch order, writes that stage
+   * (TCCD_STAGE_*) to event_stage[i] (host array, same length) and sets
+   * events_used (out).  A stage's time is the gap to the previous recorded
+   * event (the first: to an event the caller records before the call). */
+  void *const *events;
+  int32_t *event_stage;
+  int32_t n_events;
+  int32_t events_used;
+  /* Host-input overlap (ABI 3): if input_events is non-NULL, the prologue
+   * of queries [c * input_chunk, (c + 1) * input_chunk) waits for
+   * input_events[c] (cudaEvent_t recorded by the caller once those
+   * queries' inputs are on the device, e.g. after a copy on another
+   * stream); n_input_events = ceil(n / input_chunk). */
+  void *const *input_events;
+  int64_t input_chunk;
+  int32_t n_input_events;
+  int32_t reserved1;
   /* Optional compacted hit list (ABI 3): every query with status HIT
    * appends (index, toi) -- in no particular order -- at position
    * *hit_count (device u64, NOT reset by the call: zero it once and several
@@ -178,9 +193,8 @@ typedef struct tccd_batch {
   int64_t hit_index_base; /* added to every index written to hit_index (a
                              caller solving a slice of a larger batch)   */
   int64_t pool_boxes;   /* handover pool boxes per tier transition and
-                           chunk; 0 = default (tccd_workspace_bytes must
-                           be asked with the same value: see
-                           tccd_workspace_bytes_ex)                      */
+                           sub-chunk; 0 = default (tccd_workspace_bytes_ex
+                           must be asked with the same value)            */
   int64_t launches;     /* out: kernels this call launched               */
 } tccd_batch;
 

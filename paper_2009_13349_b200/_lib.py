@@ -84,6 +84,13 @@ class TccdBatch(ctypes.Structure):
         ("device_sms", ctypes.c_int32),
         ("stats", _vp),
         ("events", _vp),
+        ("event_stage", _vp),
+        ("n_events", ctypes.c_int32),
+        ("events_used", ctypes.c_int32),
+        ("input_events", _vp),
+        ("input_chunk", ctypes.c_int64),
+        ("n_input_events", ctypes.c_int32),
+        ("reserved1", ctypes.c_int32),
         ("hit_index", _vp),
         ("hit_toi", _vp),
         ("hit_count", _vp),

@@ -41,8 +41,17 @@ namespace cg = cooperative_groups;
 namespace tccd {
 
 struct Counters {
-  unsigned long long q_count[3];  // entries in the light / medium / giant queues
-  unsigned long long q_next[3];   // next entry to admit
+  // ---- per batch chunk (prologue, lane tier)
+  unsigned long long light_count;    // light-queue entries: prologue survivors + lane evictions
+  unsigned long long lane_count[2];  // lane-tier queue entries per kind (VF, EE)
+  unsigned long long lane_next[2];   // next lane entry to take per kind
+  // lane tier: [0..1] classifications VF / EE, [2..3] checks of the queries
+  // it finished (root check excluded: the prologue's), [4..5] queries
+  // finished, [6] queries evicted to the light tier, [7] their lane checks
+  unsigned long long lane[8];
+  // ---- per group-tier sub-chunk (zeroed before each)
+  unsigned long long q_count[3];  // entries in the medium / giant queues ([0] unused: light_count)
+  unsigned long long q_next[3];   // next entry to admit (light: within the sub-chunk's slice)
   unsigned long long rounds;      // engine rounds (diagnostics)
   unsigned long long deferred;    // level deferrals (diagnostics)
   unsigned long long evicted[3];  // evictions out of each tier (diagnostics)
@@ -50,28 +59,19 @@ struct Counters {
   unsigned long long pool[3];     // handover pool fill (tiers 1, 2)
   unsigned long long phase[3][16];  // cycles per engine phase (TCCD_PHASE_PROF builds)
   unsigned long long cls[3][2];   // box classifications per tier and kind (VF, EE)
-  unsigned long long lane_count[2];  // lane-tier queue entries per kind (VF, EE)
-  unsigned long long lane_next[2];   // next lane entry to take per kind
-  // lane tier: [0..1] classifications VF / EE, [2..3] checks of the queries
-  // it finished (root check excluded: the prologue's), [4..5] queries
-  // finished, [6] queries evicted to the light tier, [7] their lane checks
-  unsigned long long lane[8];
   unsigned long long restarts[3];  // evictions out of tier k that found the handover pool full
   unsigned long long algo[3];      // checks of the reference's path done per group tier (signed sum)
 };
 
-// A queued query, self-contained so a tier admits it with one coalesced
-// read: coordinates, parameters, filters and kappas, and the root class.
+// A queued query of a group tier: its index in the batch (the tier loads
+// its coordinates and recomputes its constants) and its root class.
 struct Pre {
-  double P[24];        // the 8 points (t0 block, then t1 block)
-  QueryParams qp;      // eps, kap, sep, delta, t_max, max_checks, kind
   long long q;         // query index
   double wb;           // root hull width (valid when flag says non-disjoint)
   unsigned int flag;   // root class flag (0: not classified yet)
   unsigned int pad;
 };
-static_assert(sizeof(Pre) % 8 == 0, "Pre is copied as 8-byte words");
-constexpr int kPreWords = (int)(sizeof(Pre) / 8);
+static_assert(sizeof(Pre) == 24, "Pre layout");
 
 struct Rec {  // first / drop record of a query (_kernel.py:158-171)
   Box b;
@@ -281,13 +281,7 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long
             lr.q = q;
             lr.wb = wb;
             for (int k = 0; k < 3; ++k) { lr.eps[k] = qp.eps[k]; lr.kap[k] = qp.kap[k]; }
-            lr.sep = qp.sep;
-            lr.delta = qp.delta;
-            lr.t_max = qp.t_max;
-            lr.mc = qp.max_checks;
           } else {
-            for (int k = 0; k < 24; ++k) pre.P[k] = P[k];
-            pre.qp = qp;
             pre.q = q;
             pre.wb = wb;
 #ifdef TCCD_DEBUG_ROOT_UNCLASSIFIED
@@ -330,7 +324,7 @@ namespace tccd {
 
 //                   G    NT   Q   CAP    QCAP   ADMIT  SMEM   MINB
 #ifndef TCCD_LQ
-#define TCCD_LQ 40
+#define TCCD_LQ 16
 #endif
 #ifndef TCCD_LADMIT
 #define TCCD_LADMIT 1280
@@ -387,32 +381,42 @@ using GiantCfg = EngineCfg<TCCD_GNT, TCCD_GNT, 1, 0, 0, 0, false, TCCD_GMINB>;
 template <class Cfg>
 constexpr int groups_per_cta() { return Cfg::NT / Cfg::G; }
 
-__global__ void stats_kernel(Args a, int heavy_only, long long cnt) {
+// Diagnostic counters of one group-tier sub-chunk (and, with batch != 0,
+// of the chunk's prologue and lane tier) added to the caller's stats.
+__global__ void stats_kernel(Args a, int heavy_only, long long cnt, int batch, long long sub_base,
+                             long long sub_len) {
   if (threadIdx.x == 0 && a.stats) {
     const Counters& c = *a.ctr;
     long long* S = a.stats;
-    S[TCCD_STAT_GIANT_QUERIES] += heavy_only ? (long long)c.q_count[2] : (long long)c.evicted[1];
+    const long long in_sub = (long long)c.light_count - sub_base;
+    S[TCCD_STAT_GIANT_QUERIES] +=
+        heavy_only ? (in_sub < 0 ? 0 : (in_sub < sub_len ? in_sub : sub_len)) : (long long)c.evicted[1];
     S[TCCD_STAT_ROUNDS] += (long long)c.rounds;
     S[TCCD_STAT_DEFERRALS] += (long long)c.deferred;
     S[TCCD_STAT_MEDIUM_QUERIES] += (long long)c.evicted[0];
     for (int k = 0; k < 3; ++k) S[TCCD_STAT_BOXES + k] += (long long)c.boxes[k];
-    S[TCCD_STAT_LANE_QUERIES] += (long long)(c.lane_count[0] + c.lane_count[1]);
     for (int k = 0; k < 6; ++k) S[TCCD_STAT_CLS + k] += (long long)c.cls[k / 2][k % 2];
     for (int k = 0; k < 2; ++k) {
-      S[TCCD_STAT_LANE_CLS + k] += (long long)c.lane[k];
-      S[TCCD_STAT_LANE_CHECKS + k] += (long long)c.lane[2 + k];
-      S[TCCD_STAT_LANE_DONE + k] += (long long)c.lane[4 + k];
       S[TCCD_STAT_POOL_DEMAND + k] += (long long)c.pool[1 + k];
       S[TCCD_STAT_RESTARTS + k] += (long long)c.restarts[k];
     }
-    S[TCCD_STAT_LANE_EVICTED] += (long long)c.lane[6];
-    S[TCCD_STAT_LANE_WASTED] += (long long)c.lane[7];
     for (int k = 0; k < 3; ++k) S[TCCD_STAT_TIER_CHECKS + k] += (long long)c.algo[k];
-    // survivors of the root check: the lane queue plus the prologue's light
-    // (heavy-only: giant) queue entries, which the lane tier's evictions joined
-    const unsigned long long into_light = heavy_only ? c.q_count[2] : c.q_count[0] - c.lane[6];
-    S[TCCD_STAT_PROLOGUE_DONE] += cnt - (long long)(c.lane_count[0] + c.lane_count[1] + into_light);
-    S[TCCD_STAT_CHUNKS] += 1;
+    if (batch) {
+      S[TCCD_STAT_LANE_QUERIES] += (long long)(c.lane_count[0] + c.lane_count[1]);
+      for (int k = 0; k < 2; ++k) {
+        S[TCCD_STAT_LANE_CLS + k] += (long long)c.lane[k];
+        S[TCCD_STAT_LANE_CHECKS + k] += (long long)c.lane[2 + k];
+        S[TCCD_STAT_LANE_DONE + k] += (long long)c.lane[4 + k];
+      }
+      S[TCCD_STAT_LANE_EVICTED] += (long long)c.lane[6];
+      S[TCCD_STAT_LANE_WASTED] += (long long)c.lane[7];
+      // survivors of the root check: the lane queue plus the prologue's
+      // light-queue entries (the lane tier's evictions joined that queue)
+      const unsigned long long into_light = c.light_count - c.lane[6];
+      S[TCCD_STAT_PROLOGUE_DONE] +=
+          cnt - (long long)(c.lane_count[0] + c.lane_count[1] + into_light);
+      S[TCCD_STAT_CHUNKS] += 1;
+    }
   }
 }
 
@@ -488,12 +492,21 @@ using namespace tccd;
 namespace {
 
 #ifndef TCCD_CHUNK
-#define TCCD_CHUNK (1LL << 22)
+#define TCCD_CHUNK (1LL << 26)
+#endif
+#ifndef TCCD_SUB
+#define TCCD_SUB (1LL << 23)
 #endif
 #ifndef TCCD_POOL
 #define TCCD_POOL (1LL << 25)
 #endif
-constexpr long long kChunk = TCCD_CHUNK;       // queries per host chunk
+// A call is split into chunks of at most kChunk queries: prologue and lane
+// tier over the whole chunk (one launch each: the lane tier's tail -- lanes
+// idle while the last queries finish -- is paid once per chunk), then the
+// group tiers over the chunk's light queue in sub-chunks of kSub entries
+// (their queues, handover records and pools are sized by the sub-chunk).
+constexpr long long kChunk = TCCD_CHUNK;
+constexpr long long kSub = TCCD_SUB;
 constexpr long long kPoolDefault = TCCD_POOL;  // handover pool boxes per tier transition
 
 int current_device() {
@@ -513,44 +526,51 @@ int device_sm_count(int hint) {
 long long giant_cap(long long mcmax) { return 2 * mcmax + 2; }
 
 struct Layout {
-  size_t ctr, queue[3], hand[3], pbox[3], pflag[3], perm, lq, lscratch, light, medium, giant, total;
+  size_t ctr, light_q, lq, lscratch, queue[3], hand[3], pbox[3], pflag[3], perm, light, medium,
+      giant, total;
   size_t light_b, medium_b, giant_b;
-  long long chunk, pool[3];
+  long long chunk, sub, pool[3];
   int light_blocks, medium_blocks, giant_blocks, lane_blocks;
 };
 
-// Everything scales with the chunk (min(n, kChunk) queries): queues, lane
-// scratch, one group per query at most in every tier, and handover pools no
-// larger than the chunk's largest possible handover (a query leaves the light
-// tier with at most 2 * LightCfg::QCAP boxes, the medium tier with at most
-// 2 * MediumCfg::QCAP).
+// Everything scales with the chunk (min(n, kChunk) queries) and the
+// sub-chunk (min(chunk, kSub)): queues, lane scratch, one group per query at
+// most in every tier, and handover pools no larger than the sub-chunk's
+// largest possible handover (a query leaves the light tier with at most
+// 2 * LightCfg::QCAP boxes, the medium tier with at most 2 * MediumCfg::QCAP).
 Layout layout(long long n, long long mcmax, int giant_blocks, int sms, long long pool_boxes) {
   Layout L;
   const long long chunk = n < kChunk ? (n > 0 ? n : 1) : kChunk;
+  const long long sub = chunk < kSub ? chunk : kSub;
   L.chunk = chunk;
+  L.sub = sub;
   const long long pool = pool_boxes > 0 ? pool_boxes : kPoolDefault;
   L.pool[0] = 0;
-  L.pool[1] = std::min(pool, chunk * 2 * LightCfg::QCAP);
-  L.pool[2] = std::min(pool, chunk * 2 * MediumCfg::QCAP);
+  L.pool[1] = std::min(pool, sub * 2 * LightCfg::QCAP);
+  L.pool[2] = std::min(pool, sub * 2 * MediumCfg::QCAP);
   L.lane_blocks = (int)std::min<long long>((long long)TCCD_NMINB * sms, (chunk + kLaneNT - 1) / kLaneNT);
-  L.light_blocks = (int)std::min<long long>((long long)TCCD_LMINB * sms, chunk);
-  L.medium_blocks = (int)std::min<long long>((long long)MediumCfg::MINB * sms, chunk);
-  L.giant_blocks = (int)std::min<long long>(giant_blocks, chunk);
+  L.light_blocks = (int)std::min<long long>((long long)TCCD_LMINB * sms, sub);
+  L.medium_blocks = (int)std::min<long long>((long long)MediumCfg::MINB * sms, sub);
+  L.giant_blocks = (int)std::min<long long>(giant_blocks, sub);
   L.light_b = align256(EngineArena<LightCfg>::bytes(LightCfg::CAP));
   L.medium_b = align256(EngineArena<MediumCfg>::bytes(MediumCfg::CAP));
   L.giant_b = align256(EngineArena<GiantCfg>::bytes(giant_cap(mcmax)));
   size_t o = 0;
   L.ctr = o; o += align256(sizeof(Counters));
-  for (int k = 0; k < 3; ++k) { L.queue[k] = o; o += align256((size_t)chunk * sizeof(Pre)); }
+  // per chunk
+  L.light_q = o; o += align256((size_t)chunk * sizeof(Pre));
+  L.lq = o; o += align256((size_t)chunk * sizeof(LaneRec));
+  L.lscratch = o; o += align256((size_t)L.lane_blocks * kLaneNT * kLaneScratchWords * 8);
+  // per sub-chunk
+  L.queue[0] = L.light_q;
   L.hand[0] = L.pbox[0] = L.pflag[0] = 0;
   for (int k = 1; k < 3; ++k) {
-    L.hand[k] = o; o += align256((size_t)chunk * sizeof(Hand));
+    L.queue[k] = o; o += align256((size_t)sub * sizeof(Pre));
+    L.hand[k] = o; o += align256((size_t)sub * sizeof(Hand));
     L.pbox[k] = o; o += align256((size_t)L.pool[k] * sizeof(Box));
     L.pflag[k] = o; o += align256((size_t)L.pool[k]);
   }
   L.perm = o; o += align256((size_t)kOrderMax * 4);
-  L.lq = o; o += align256((size_t)chunk * sizeof(LaneRec));
-  L.lscratch = o; o += align256((size_t)L.lane_blocks * kLaneNT * 3 * kLaneCap * 8);
   L.light = o; o += L.light_b * (size_t)L.light_blocks * groups_per_cta<LightCfg>();
   L.medium = o; o += L.medium_b * (size_t)L.medium_blocks * groups_per_cta<MediumCfg>();
   L.giant = o; o += L.giant_b * (size_t)L.giant_blocks;
@@ -664,6 +684,7 @@ int tccd_solve_batch(const tccd_batch* b_in, void* stream) {
   if (b_in->struct_size != sizeof(tccd_batch)) return TCCD_E_STRUCT;
   tccd_batch* out_b = const_cast<tccd_batch*>(b_in);
   out_b->launches = 0;
+  out_b->events_used = 0;
   const tccd_batch* b = b_in;
   if (b->n < 0) return TCCD_E_N;
   if (b->n > 0 && (!b->points || !b->status || !b->toi)) return TCCD_E_NULL;
@@ -725,34 +746,46 @@ int tccd_solve_batch(const tccd_batch* b_in, void* stream) {
 
   Pre* queue[3];
   for (int k = 0; k < 3; ++k) queue[k] = (Pre*)(ws + L.queue[k]);
-  auto io_for = [&](int tier) {
+  Counters* const ctr = a.ctr;
+  // group tier `tier` over sub-chunk `sub` of the chunk's light queue
+  auto io_for = [&](int tier, long long sub) {
     TierIO io;
-    io.in = queue[tier];
-    // (in heavy-only mode the prologue feeds the giant tier: no handovers)
+    // (heavy-only: the giant tier reads the prologue's queue directly)
+    const bool from_light = tier == 0 || a.heavy_only;
+    io.in = from_light ? queue[0] : queue[tier];
+    io.in_count = from_light ? &ctr->light_count : &ctr->q_count[tier];
+    io.in_base = from_light ? sub * L.sub : 0;
+    io.in_limit = from_light ? L.sub : (long long)(1ull << 62);
+    io.in_next = &ctr->q_next[tier];
     io.in_hand = tier > 0 && !a.heavy_only ? (const Hand*)(ws + L.hand[tier]) : nullptr;
     io.in_pbox = tier > 0 ? (const Box*)(ws + L.pbox[tier]) : nullptr;
     io.in_pflag = tier > 0 ? (const uint8_t*)(ws + L.pflag[tier]) : nullptr;
-    io.in_maxsz = tier == 0 ? 1 : 2 * (tier == 1 ? LightCfg::QCAP : MediumCfg::QCAP);
+    io.in_pool_cap = L.pool[tier];
+    // (light tier: the lane tier's evictions restart there and are known to
+    // reach levels above kLaneCap boxes: admit them as if they had that many)
+#ifndef TCCD_LIGHT_MAXSZ
+#define TCCD_LIGHT_MAXSZ 1
+#endif
+    io.in_maxsz = a.heavy_only ? 1
+                  : (tier == 0 ? (lanes ? TCCD_LIGHT_MAXSZ : 1)
+                               : 2 * (tier == 1 ? LightCfg::QCAP : MediumCfg::QCAP));
     io.in_perm = tier == 2 && !a.heavy_only ? (const unsigned int*)(ws + L.perm) : nullptr;
     io.perm_max = kOrderMax;
     io.out_hand = tier < 2 ? (Hand*)(ws + L.hand[tier + 1]) : nullptr;
     io.out_pbox = tier < 2 ? (Box*)(ws + L.pbox[tier + 1]) : nullptr;
     io.out_pflag = tier < 2 ? (uint8_t*)(ws + L.pflag[tier + 1]) : nullptr;
-    io.out_pool_count = tier < 2 ? &a.ctr->pool[tier + 1] : nullptr;
+    io.out_pool_count = tier < 2 ? &ctr->pool[tier + 1] : nullptr;
     io.pool_cap = tier < 2 ? L.pool[tier + 1] : 0;
-    io.in_pool_cap = L.pool[tier];
-    io.in_count = &a.ctr->q_count[tier];
-    io.in_next = &a.ctr->q_next[tier];
     io.out = tier < 2 ? queue[tier + 1] : nullptr;
-    io.out_count = tier < 2 ? &a.ctr->q_count[tier + 1] : nullptr;
-    io.rounds = &a.ctr->rounds;
-    io.deferred = &a.ctr->deferred;
-    io.evicted = &a.ctr->evicted[tier];
-    io.boxes = &a.ctr->boxes[tier];
-    io.phase = a.ctr->phase[tier];
-    io.cls = a.ctr->cls[tier];
-    io.restarts = &a.ctr->restarts[tier];
-    io.algo = &a.ctr->algo[tier];
+    io.out_count = tier < 2 ? &ctr->q_count[tier + 1] : nullptr;
+    io.rounds = &ctr->rounds;
+    io.deferred = &ctr->deferred;
+    io.evicted = &ctr->evicted[tier];
+    io.boxes = &ctr->boxes[tier];
+    io.phase = ctr->phase[tier];
+    io.cls = ctr->cls[tier];
+    io.restarts = &ctr->restarts[tier];
+    io.algo = &ctr->algo[tier];
     if (tier == 0) { io.arenas = ws + L.light; io.arena_bytes = L.light_b; io.cap = LightCfg::CAP; }
     if (tier == 1) { io.arenas = ws + L.medium; io.arena_bytes = L.medium_b; io.cap = MediumCfg::CAP; }
     if (tier == 2) { io.arenas = ws + L.giant; io.arena_bytes = L.giant_b; io.cap = giant_cap(mcmax); }
@@ -761,65 +794,87 @@ int tccd_solve_batch(const tccd_batch* b_in, void* stream) {
   LaneIO lio;
   lio.rec = (const LaneRec*)(ws + L.lq);
   lio.rec_cap = L.chunk;
-  lio.count = a.ctr->lane_count;
-  lio.next = a.ctr->lane_next;
+  lio.count = ctr->lane_count;
+  lio.next = ctr->lane_next;
   lio.scratch = (unsigned long long*)(ws + L.lscratch);
   lio.out = queue[0];
-  lio.out_count = &a.ctr->q_count[0];
-  lio.stats = a.ctr->lane;
+  lio.out_count = &ctr->light_count;
+  lio.stats = ctr->lane;
 
-  // optional caller events, recorded after each stage of every chunk
-  auto mark = [&](int k) {
-    return b->events && b->events[k] ? cudaEventRecord((cudaEvent_t)b->events[k], st) : cudaSuccess;
+  // optional caller events, one after each stage launch, in launch order
+  int n_ev = 0;
+  auto mark = [&](int stage) {
+    if (!b->events || n_ev >= b->n_events) return cudaSuccess;
+    const cudaError_t e = cudaEventRecord((cudaEvent_t)b->events[n_ev], st);
+    if (b->event_stage) b->event_stage[n_ev] = stage;
+    ++n_ev;
+    return e;
   };
+  const size_t sub_off = offsetof(Counters, q_count);
   long long launches = 0;
   for (long long lo = 0; lo < b->n; lo += kChunk) {
     const long long cnt = b->n - lo < kChunk ? b->n - lo : kChunk;
-    if (cudaMemsetAsync(a.ctr, 0, sizeof(Counters), st) != cudaSuccess) return TCCD_E_CUDA;
-#ifdef TCCD_PHASE_PROF
-    for (int k = 0; k < 3; ++k)  // phase[k][14] is a running min (start time)
-      if (cudaMemsetAsync(&a.ctr->phase[k][14], 0xFF, 8, st) != cudaSuccess) return TCCD_E_CUDA;
-#endif
-    const int first = a.heavy_only ? 2 : 0;
-    const unsigned pblocks = (unsigned)((cnt + kPrologueThreads - 1) / kPrologueThreads);
-    prologue_kernel<<<pblocks, kPrologueThreads, 0, st>>>(
-        a, lo, cnt, queue[first], &a.ctr->q_count[first],
-        lanes ? (LaneRec*)(ws + L.lq) : nullptr, L.chunk, a.ctr->lane_count);
-    ++launches;
-    if (cudaGetLastError() != cudaSuccess || mark(TCCD_STAGE_PROLOGUE) != cudaSuccess)
-      return TCCD_E_CUDA;
+    if (cudaMemsetAsync(ctr, 0, sizeof(Counters), st) != cudaSuccess) return TCCD_E_CUDA;
+    // prologue, one launch per input-ready piece (the whole chunk without
+    // input events)
+    const long long piece = b->input_events && b->input_chunk > 0 ? b->input_chunk : cnt;
+    for (long long p0 = lo; p0 < lo + cnt; p0 += piece) {
+      const long long pc = std::min(piece, lo + cnt - p0);
+      if (b->input_events) {
+        const long long c = p0 / b->input_chunk;
+        if (c < b->n_input_events && b->input_events[c] &&
+            cudaStreamWaitEvent(st, (cudaEvent_t)b->input_events[c], 0) != cudaSuccess)
+          return TCCD_E_CUDA;
+      }
+      const unsigned pblocks = (unsigned)((pc + kPrologueThreads - 1) / kPrologueThreads);
+      prologue_kernel<<<pblocks, kPrologueThreads, 0, st>>>(
+          a, p0, pc, queue[0], &ctr->light_count, lanes ? (LaneRec*)(ws + L.lq) : nullptr,
+          L.chunk, ctr->lane_count);
+      ++launches;
+      if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
+    }
+    if (mark(TCCD_STAGE_PROLOGUE) != cudaSuccess) return TCCD_E_CUDA;
     if (lanes) {
       lane_kernel<<<L.lane_blocks, kLaneNT, 0, st>>>(a, lio);
       ++launches;
-      if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
+      if (cudaGetLastError() != cudaSuccess || mark(TCCD_STAGE_LANE) != cudaSuccess)
+        return TCCD_E_CUDA;
     }
-    if (mark(TCCD_STAGE_LANE) != cudaSuccess) return TCCD_E_CUDA;
-    int rc;
-    if (!a.heavy_only) {
-      if ((rc = launch_tier<LightCfg>(a, io_for(0), L.light_blocks, st)) != TCCD_OK) return rc;
+    // group tiers over the light queue, sub-chunk by sub-chunk (a sub-chunk
+    // past the queue's end exits at once: the count is only known on the device)
+    const long long nsub = (cnt + L.sub - 1) / L.sub;
+    for (long long sub = 0; sub < nsub; ++sub) {
+      if (cudaMemsetAsync((unsigned char*)ctr + sub_off, 0, sizeof(Counters) - sub_off, st) !=
+          cudaSuccess)
+        return TCCD_E_CUDA;
+#ifdef TCCD_PHASE_PROF
+      for (int k = 0; k < 3; ++k)  // phase[k][14] is a running min (start time)
+        if (cudaMemsetAsync(&ctr->phase[k][14], 0xFF, 8, st) != cudaSuccess) return TCCD_E_CUDA;
+#endif
+      int rc;
+      if (!a.heavy_only) {
+        if ((rc = launch_tier<LightCfg>(a, io_for(0, sub), L.light_blocks, st)) != TCCD_OK) return rc;
+        ++launches;
+        if (mark(TCCD_STAGE_LIGHT) != cudaSuccess) return TCCD_E_CUDA;
+        if ((rc = launch_tier<MediumCfg>(a, io_for(1, sub), L.medium_blocks, st)) != TCCD_OK) return rc;
+        ++launches;
+        if (mark(TCCD_STAGE_MEDIUM) != cudaSuccess) return TCCD_E_CUDA;
+        order_kernel<<<1, 1024, 0, st>>>((const Hand*)(ws + L.hand[2]), &ctr->q_count[2],
+                                         (unsigned int*)(ws + L.perm));
+        ++launches;
+        if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
+      }
+      if ((rc = launch_tier<GiantCfg>(a, io_for(2, sub), L.giant_blocks, st)) != TCCD_OK) return rc;
       ++launches;
-      if (mark(TCCD_STAGE_LIGHT) != cudaSuccess) return TCCD_E_CUDA;
-      if ((rc = launch_tier<MediumCfg>(a, io_for(1), L.medium_blocks, st)) != TCCD_OK) return rc;
-      ++launches;
-      if (mark(TCCD_STAGE_MEDIUM) != cudaSuccess) return TCCD_E_CUDA;
-    } else if (mark(TCCD_STAGE_LIGHT) != cudaSuccess || mark(TCCD_STAGE_MEDIUM) != cudaSuccess) {
-      return TCCD_E_CUDA;
-    }
-    if (!a.heavy_only) {
-      order_kernel<<<1, 1024, 0, st>>>((const Hand*)(ws + L.hand[2]), &a.ctr->q_count[2],
-                                       (unsigned int*)(ws + L.perm));
-      ++launches;
-      if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
-    }
-    if ((rc = launch_tier<GiantCfg>(a, io_for(2), L.giant_blocks, st)) != TCCD_OK) return rc;
-    ++launches;
-    if (mark(TCCD_STAGE_GIANT) != cudaSuccess) return TCCD_E_CUDA;
-    if (a.stats) {
-      stats_kernel<<<1, 32, 0, st>>>(a, a.heavy_only, cnt);
-      ++launches;
-      if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
+      if (mark(TCCD_STAGE_GIANT) != cudaSuccess) return TCCD_E_CUDA;
+      if (a.stats) {
+        stats_kernel<<<1, 32, 0, st>>>(a, a.heavy_only, cnt, sub == 0 ? 1 : 0, sub * L.sub, L.sub);
+        ++launches;
+        if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
+      }
     }
   }
+  out_b->events_used = n_ev;
   out_b->launches = launches;
   return TCCD_OK;
 }

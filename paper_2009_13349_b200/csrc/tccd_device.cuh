@@ -154,6 +154,39 @@ __device__ __forceinline__ int classify_k(PtrT P, const Box& b, const double* ep
   return contained ? kContained : kIntersects;
 }
 
+// The same classification with all three axes evaluated (tame coordinates):
+// the reference returns at the first separated axis, but the class and wb it
+// returns do not depend on which axis that was (DISJOINT, wb = 0), and for a
+// non-disjoint box it has evaluated all three.  A warp pays for the three
+// axes as soon as one lane's box is not separated on the first, so the
+// branch-free form costs the warp no flops and lets the three hulls
+// interleave.  EpsT indexes like an array (pointer or strided accessor).
+template <int KIND, typename PtrT, typename EpsT>
+__device__ __forceinline__ int classify_full(PtrT P, const Box& b, EpsT eps, double sep,
+                                             double& wb) {
+  const CornerWeights w = corner_weights(b);
+  const double omt0 = 1.0 - b.t0, omt1 = 1.0 - b.t1;
+  bool disjoint = false, contained = true;
+  double width = 0.0;
+#ifdef TCCD_FULL_UNROLL
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+  for (int ax = 0; ax < 3; ++ax) {
+    double mn, mx;
+    hull_axis<KIND, true>(P, ax, b.t0, omt0, b.t1, omt1, w, mn, mx);
+    const double e = eps[ax];
+    const double lo = mn - sep, hi = mx + sep;
+    disjoint |= lo > e || hi < -e;
+    contained &= lo >= -e && hi <= e;
+    const double d = mx - mn;
+    width = d > width ? d : width;
+  }
+  wb = disjoint ? 0.0 : width;
+  return disjoint ? kDisjoint : (contained ? kContained : kIntersects);
+}
+
 template <typename PtrT>
 __device__ __forceinline__ int classify(PtrT P, int kind, const Box& b, const double* eps,
                                         double sep, double& wb, bool tame = false) {

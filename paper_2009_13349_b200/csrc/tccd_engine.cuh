@@ -421,6 +421,8 @@ struct TierIO {
   long long pool_cap;
   unsigned long long* in_count;
   unsigned long long* in_next;
+  long long in_base;        // this launch's slice of the input queue
+  long long in_limit;
   long long in_pool_cap;    // boxes in the input handover pool
   Pre* out;                 // eviction queue of the next tier (nullptr: none)
   unsigned long long* out_count;
@@ -471,7 +473,13 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   const int cap = Cfg::CAP ? Cfg::CAP : (int)io.cap;
   const int qcap = Cfg::QCAP ? Cfg::QCAP : cap;
   const int admit_lim = Cfg::ADMIT ? Cfg::ADMIT : cap;
-  const unsigned long long in_total = *(volatile unsigned long long*)io.in_count;
+  // this launch's slice of the input queue: entries [in_base, in_base + in_limit)
+  const unsigned long long in_all = *(volatile unsigned long long*)io.in_count;
+  const unsigned long long in_total =
+      in_all <= (unsigned long long)io.in_base ? 0ull
+      : (in_all - io.in_base < (unsigned long long)io.in_limit ? in_all - io.in_base
+                                                               : (unsigned long long)io.in_limit);
+  const Pre* const inq = io.in + io.in_base;
   // queue entry admitted at position k
   const bool use_perm = io.in_perm && in_total >= 2 && (long long)in_total <= io.perm_max;
   auto entry = [&](long long k) -> long long { return use_perm ? (long long)io.in_perm[k] : k; };
@@ -497,12 +505,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   // the next tier resumes the query; otherwise it restarts from the root.
   auto evict = [&](int s, int t) {
     const unsigned long long h = atomicAdd(io.out_count, 1ull);
-    Pre& p = io.out[h];
-    for (int k = 0; k < 24; ++k) p.P[k] = S.P[s][k];
-    p.qp = S.qp[s];
-    p.q = S.qidx[s];
-    p.wb = 0.0;
-    p.flag = 0;
+    io.out[h] = Pre{S.qidx[s], 0.0, 0u, 0u};
     long long off = -1;
     if (io.out_hand) {
       const unsigned long long o = atomicAdd(io.out_pool_count, (unsigned long long)t);
@@ -597,24 +600,42 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       }
     }
     gsync<G>();
-    // step 1b: warp-cooperative copy of the queue records (one coalesced read)
+    // step 1b: the queue records (query index, root class) and, warp-
+    // cooperatively, the query's 24 coordinates from the batch (192 bytes,
+    // coalesced)
     {
       constexpr int NWARP = (NT + 31) / 32;
       const int wid = tid >> 5, lane = tid & 31;
       for (int r = wid; r < k_adm; r += NWARP) {
         const int s = S.adm_slot[r];
-        const unsigned long long* src =
-            reinterpret_cast<const unsigned long long*>(io.in + entry(S.admit_base + r));
-        for (int wd = lane; wd < kPreWords; wd += 32) {
-          const unsigned long long v = src[wd];
-          if (wd < 24) reinterpret_cast<unsigned long long*>(S.P[s])[wd] = v;
-          else if (wd < 24 + (int)(sizeof(QueryParams) / 8))
-            reinterpret_cast<unsigned long long*>(&S.qp[s])[wd - 24] = v;
-          else if (wd == (int)(offsetof(Pre, q) / 8)) S.qidx[s] = (long long)v;
-          else if (wd == (int)(offsetof(Pre, wb) / 8)) S.root_wb[s] = __longlong_as_double(v);
-          else if (wd == (int)(offsetof(Pre, flag) / 8)) S.root_flag[s] = (uint8_t)(v & 0xffu);
+        const Pre& e = inq[entry(S.admit_base + r)];
+        const long long q = e.q;
+        if (lane < 24) S.P[s][lane] = a.points[24 * q + lane];
+        if (lane == 0) {
+          S.qidx[s] = q;
+          S.root_wb[s] = e.wb;
+          S.root_flag[s] = (uint8_t)(e.flag & 0xffu);
         }
       }
+    }
+    gsync<G>();
+    // step 1b': per-query constants, recomputed from the coordinates exactly
+    // as the prologue did (parameters, filters, kappas): a queue record is an
+    // index, not a copy
+    for (int r = tid; r < k_adm; r += NT) {
+      const int s = S.adm_slot[r];
+      const long long q = S.qidx[s];
+      QueryParams qp;
+      load_params(a, q, qp);
+      const double* P = S.P[s];
+      if (a.eps) {
+        qp.eps[0] = a.eps[3 * q]; qp.eps[1] = a.eps[3 * q + 1]; qp.eps[2] = a.eps[3 * q + 2];
+      } else {
+        filters(P, qp.kind, qp.sep, qp.eps);  // (valid: the prologue checked it)
+      }
+      qp.tame = tame_coords(P);
+      kappas(P, qp.kind, qp.t_max, qp.kap);
+      S.qp[s] = qp;
     }
     gsync<G>();
     // step 1c: per-slot state (fresh root, or a level handed over by the

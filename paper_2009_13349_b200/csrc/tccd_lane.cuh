@@ -20,10 +20,18 @@
 // is one 64-bit word ti | ui | vi (v in the low bits), a child inserts one
 // bit at its split dimension's position.  A level's refining boxes all split
 // along one dimension (same widths, same kappas), so its children are
-// written in the order the reference's stable t_lo sort gives them: push
-// order for u / v splits; for a t split, per run of equal parent t_lo, all
-// lower children then all upper children (the uppers wait in a third array
-// until the run ends).
+// visited in the order the reference's stable t_lo sort gives them: push
+// order after a u / v split; after a t split, per run of equal parent t_lo,
+// all lower children then all upper children.  Children are stored in push
+// order (lower, upper, lower, upper, ...) with the length of each parent
+// run's segment, and a t-split level's successor is visited segment by
+// segment, even positions first: no box is ever moved.
+//
+// Latency: the word of the next box is loaded while the current box is
+// classified; a lane that takes a new query copies its 64-byte record
+// (index, filters, kappas) and then the query's coordinates and parameters
+// into its shared-memory column with cp.async, one iteration apart, and
+// starts on it the iteration after, so neither stalls the warp.
 //
 // A query leaves this tier (and restarts from its root in the light tier:
 // exact, classification is a pure function of the box) when a level would
@@ -39,47 +47,64 @@ namespace tccd {
 #define TCCD_NNT 128
 #endif
 #ifndef TCCD_NMINB
-#define TCCD_NMINB 4
+#define TCCD_NMINB 3
 #endif
 constexpr int kLaneCap = TCCD_KL;  // boxes per level of a lane query
 constexpr int kLaneNT = TCCD_NNT;  // threads per CTA
 constexpr int kLaneMaxSplits = 52;  // per dimension: midpoints stay exact (indices < 2^53)
 constexpr int kLaneMaxLevel = 62;   // ti | ui | vi fits one 64-bit word
+// per-lane global scratch: two level arrays of words and two segment tables
+constexpr int kLaneSeg = kLaneCap / 2;
+constexpr int kLaneScratchWords = 2 * kLaneCap + kLaneSeg;  // (segment tables: 2 x u32 per word)
 
 // A query queued for the lane tier by the prologue: its root box is
-// non-disjoint and refined (one check done).
+// non-disjoint and refined (one check done); its filters and kappas.
 struct LaneRec {
   long long q;
   double wb;  // root hull width (the first record's codomain width)
   double eps[3];
   double kap[3];
-  double sep, delta, t_max;
-  long long mc;
 };
-static_assert(sizeof(LaneRec) == 96, "LaneRec layout");
+static_assert(sizeof(LaneRec) == 64, "LaneRec layout");
+// shared-memory column of one lane: the 24 coordinates, the LaneRec words,
+// the per-query parameters
+constexpr int kLaneCol = 36;
+constexpr int kColQ = 24, kColWb = 25, kColEps = 26, kColKap = 29, kColSep = 32, kColDelta = 33,
+              kColTmax = 34, kColMc = 35;
 
 struct LaneIO {
   const LaneRec* rec;             // vertex-face entries from the front, edge-edge from the back
   long long rec_cap;
   const unsigned long long* count;  // [2] entries per kind
   unsigned long long* next;         // [2] next entry to take per kind
-  unsigned long long* scratch;      // [grid threads][3][kLaneCap] level words
+  unsigned long long* scratch;      // [grid threads][kLaneScratchWords]
   Pre* out;                         // light-tier queue (evicted queries restart there)
   unsigned long long* out_count;
   unsigned long long* stats;        // [8] see Counters::lane
 };
 
-// this thread's query coordinates: one column of a [24][NT] shared array
+// this thread's column of a [kLaneCol][NT] shared array, read like an array
 template <int NT>
 struct ColP {
   const double* p;
   __device__ __forceinline__ double operator[](int k) const { return p[k * NT]; }
 };
 
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // box of lattice word pk at split counts (nt, nu, nv)
 __device__ __forceinline__ Box lane_box(unsigned long long pk, int nt, int nu, int nv,
                                         double t_max) {
-  const double wt = ldexp(t_max, -nt), wu = ldexp(1.0, -nu), wv = ldexp(1.0, -nv);
+  // 2^-n (n <= 62) built from its exponent bits: exact, no ldexp call
+  const double wt = t_max * __longlong_as_double((long long)(1023 - nt) << 52);
+  const double wu = __longlong_as_double((long long)(1023 - nu) << 52);
+  const double wv = __longlong_as_double((long long)(1023 - nv) << 52);
   const unsigned long long ti = pk >> (nu + nv);
   const unsigned long long ui = (pk >> nv) & ((1ull << nu) - 1ull);
   const unsigned long long vi = pk & ((1ull << nv) - 1ull);
@@ -92,7 +117,8 @@ __device__ __forceinline__ Box lane_box(unsigned long long pk, int nt, int nu, i
 
 // split dimension of a level whose boxes have widths (wt, wu, wv)
 // (_kernel.py:219-229: strict >, ties to t, then u)
-__device__ __forceinline__ int lane_split_dim(double wt, double wu, double wv, const double* kap) {
+template <typename KapT>
+__device__ __forceinline__ int lane_split_dim(double wt, double wu, double wv, KapT kap) {
   const double ct = wt * kap[0], cu = wu * kap[1], cv = wv * kap[2];
   int sd = 0;
   double best = ct;
@@ -120,223 +146,299 @@ __device__ __forceinline__ void lane_write(const Args& a, long long q, bool use_
   write_result(a, q, kHit, b, use_x ? x.codom : y.codom, checks, early, use_x ? x.level : y.level);
 }
 
+struct LaneStats {
+  unsigned long long cls = 0, checks = 0, done = 0, evicted = 0, wasted = 0;
+};
+
 template <int KIND>
-__device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, double* colbase,
-                                          unsigned long long* lb, unsigned long long (&st)[8]) {
+__device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, double* col,
+                                          unsigned long long* lb, LaneStats& st) {
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const ColP<kLaneNT> P{colbase};
+  const ColP<kLaneNT> P{col};
+  const ColP<kLaneNT> eps{col + kColEps * kLaneNT};
+  const ColP<kLaneNT> kap{col + kColKap * kLaneNT};
+  unsigned int* const segs = reinterpret_cast<unsigned int*>(lb + 2 * kLaneCap);  // [2][kLaneSeg]
   const unsigned long long total = io.count[KIND];
-  bool dry = false;    // (warp-uniform) this kind's queue is empty
-  bool active = false;
+  bool dry = false;  // (warp-uniform) this kind's queue is empty
+  int state = 0;     // 0 idle, 1 record in flight, 2 coordinates in flight, 3 active
   // query
   long long q = 0, mc = 0, C = 0;
-  double eps[3] = {0, 0, 0}, kap[3] = {0, 0, 0}, sep = 0, delta = 0, t_max = 1;
-  // level
-  int L = 0, nt = 0, nu = 0, nv = 0, sd = 0, ncur = 0, icur = 0, nn = 0, ntmp = 0, cb = 0;
+  double sep = 0, delta = 0, t_max = 1;
+  double kapr[3] = {0, 0, 0};  // kappas (registers: every level end reads them)
+  // level: split counts and widths of its boxes, its split dimension
+  int L = 0, nt = 0, nu = 0, nv = 0, sd = 0;
   double wt = 1, wu = 1, wv = 1;
-  bool col = false;
-  unsigned long long run = ~0ull;
+  int cb = 0;        // current level array: lb + cb (the next one: lb + (cb ^ kLaneCap))
+  int sgb = 0;       // current segment table: segs + sgb (the next one: segs + (sgb ^ kLaneSeg))
+  int ncur = 0, k = 0;
+  // visiting order of the current level: identity, or (after a t split)
+  // segment by segment, even positions first
+  bool ilv = false;
+  int seg_start = 0, seg_m = 0, seg_k = 0, seg_i = 0, seg_mn = 0, nseg = 0;
+  unsigned long long pk = 0, pk_next = 0;
+  // next level: children written, segments closed, the current run (t split)
+  int nn = 0, nsn = 0, run_m = 0, seg0 = 0;
+  unsigned long long run = ~0ull, nxt0 = 0;
+  bool col_lvl = false;  // this level has had a non-disjoint box (last_colliding_level)
   LaneRecBox fr{}, dr{};
   bool hf = false, hd = false;
 
   for (;;) {
-    // ---- refill idle lanes (warp-aggregated claim)
-    const unsigned need = __ballot_sync(FULL, !active);
+    // ---- idle lanes claim a query (warp-aggregated) and start its copy
+    const unsigned need = __ballot_sync(FULL, state == 0);
     if (need && !dry) {
       const int leader = __ffs(need) - 1;
       unsigned long long base = 0;
       if (lane == leader) base = atomicAdd(&io.next[KIND], (unsigned long long)__popc(need));
       base = __shfl_sync(FULL, base, leader);
       if (base + __popc(need) >= total) dry = true;
-      if (!active) {
-        const unsigned long long k = base + __popc(need & ((1u << lane) - 1u));
-        if (k < total) {
-          const LaneRec& r = io.rec[KIND ? io.rec_cap - 1 - (long long)k : (long long)k];
-          q = r.q;
-          const double2* src = reinterpret_cast<const double2*>(a.points + 24 * q);
+      if (state == 0) {
+        const unsigned long long kq = base + __popc(need & ((1u << lane) - 1u));
+        if (kq < total) {
+          const double* src = reinterpret_cast<const double*>(
+              &io.rec[KIND ? io.rec_cap - 1 - (long long)kq : (long long)kq]);
 #pragma unroll
-          for (int i = 0; i < 12; ++i) {
-            const double2 v = src[i];
-            colbase[(2 * i) * kLaneNT] = v.x;
-            colbase[(2 * i + 1) * kLaneNT] = v.y;
-          }
-          eps[0] = r.eps[0]; eps[1] = r.eps[1]; eps[2] = r.eps[2];
-          kap[0] = r.kap[0]; kap[1] = r.kap[1]; kap[2] = r.kap[2];
-          sep = r.sep; delta = r.delta; t_max = r.t_max; mc = r.mc;
-          // the root (level 0, one check, the prologue's) is the first record
-          // and was refined: level 1 = its two children (a root child is
-          // never clipped: mid + 0 <= 1)
-          fr.pk = 0; fr.shape = 0; fr.level = 0; fr.codom = r.wb; fr.t0 = 0.0;
-          hf = true; hd = false;
-          C = 1;
-          nt = nu = nv = 0;
-          wt = t_max; wu = 1.0; wv = 1.0;
-          const int s0 = lane_split_dim(wt, wu, wv, kap);
-          if (s0 == 0) { nt = 1; wt *= 0.5; } else if (s0 == 1) { nu = 1; wu *= 0.5; } else { nv = 1; wv *= 0.5; }
-          cb = 0;
-          lb[0] = 0ull;
-          lb[1] = 1ull;
-          ncur = 2; icur = 0; nn = 0; ntmp = 0;
-          L = 1;
-          col = false;
-          run = ~0ull;
-          sd = lane_split_dim(wt, wu, wv, kap);
-          active = true;
+          for (int i = 0; i < 8; ++i) cp_async8(col + (kColQ + i) * kLaneNT, src + i);
+          state = 1;
         }
       }
     }
-    if (!__any_sync(FULL, active)) break;
-    if (!active) continue;
+    if (!__any_sync(FULL, state != 0)) break;
+    if (state == 1) {
+      // the record has landed (one iteration later): copy the coordinates
+      // and the per-query parameters
+      cp_async_wait_all();
+      const long long qn = __double_as_longlong(col[kColQ * kLaneNT]);
+      const double* src = a.points + 24 * qn;
+#pragma unroll
+      for (int i = 0; i < 24; ++i) cp_async8(col + i * kLaneNT, src + i);
+      if (a.sep) cp_async8(col + kColSep * kLaneNT, a.sep + qn);
+      else col[kColSep * kLaneNT] = a.sep_all;
+      if (a.delta) cp_async8(col + kColDelta * kLaneNT, a.delta + qn);
+      else col[kColDelta * kLaneNT] = a.delta_all;
+      if (a.t_max) cp_async8(col + kColTmax * kLaneNT, a.t_max + qn);
+      else col[kColTmax * kLaneNT] = a.t_max_all;
+      if (a.max_checks) cp_async8(col + kColMc * kLaneNT, reinterpret_cast<const double*>(a.max_checks + qn));
+      else col[kColMc * kLaneNT] = __longlong_as_double(a.max_checks_all);
+      state = 2;
+      continue;
+    }
+    if (state == 2) {
+      cp_async_wait_all();
+      q = __double_as_longlong(col[kColQ * kLaneNT]);
+      mc = __double_as_longlong(col[kColMc * kLaneNT]);
+      sep = col[kColSep * kLaneNT];
+      delta = col[kColDelta * kLaneNT];
+      t_max = col[kColTmax * kLaneNT];
+      kapr[0] = kap[0]; kapr[1] = kap[1]; kapr[2] = kap[2];
+      // the root (level 0, one check, the prologue's) is the first record
+      // and was refined: level 1 = its two children (never clipped: a root
+      // child's lower corner is 0)
+      fr.pk = 0; fr.shape = 0; fr.level = 0; fr.codom = col[kColWb * kLaneNT]; fr.t0 = 0.0;
+      hf = true; hd = false;
+      C = 1;
+      nt = nu = nv = 0;
+      wt = t_max; wu = 1.0; wv = 1.0;
+      const int s0 = lane_split_dim(wt, wu, wv, kapr);
+      if (s0 == 0) { nt = 1; wt *= 0.5; } else if (s0 == 1) { nu = 1; wu *= 0.5; } else { nv = 1; wv *= 0.5; }
+      cb = 0; sgb = 0;
+      lb[0] = 0ull;
+      lb[1] = 1ull;
+      ncur = 2; k = 0; L = 1;
+      // (a t split of the root leaves one run of one parent: order 0, 1 either way)
+      ilv = false; seg_start = 0; seg_m = 0; seg_k = 0; seg_i = 0; seg_mn = 0; nseg = 0;
+      pk = 0; pk_next = 1;
+      nn = 0; nsn = 0; run_m = 0; seg0 = 0; run = ~0ull; nxt0 = 0;
+      col_lvl = false;
+      sd = lane_split_dim(wt, wu, wv, kapr);
+      state = 3;
+    }
+    if (state != 3) continue;  // (idle: this kind's queue ran dry)
 
-    // ---- one box of the current level, in visiting order
+    // ---- one box of the current level, in visiting order.  The bookkeeping
+    // is written as selects and predicated stores, so the lanes of a warp --
+    // each somewhere else in its own query -- run it together; only the
+    // writes of a finished query branch.
     unsigned long long* const cur = lb + cb;
     unsigned long long* const nxt = lb + (cb ^ kLaneCap);
-    unsigned long long* const tmp = lb + 2 * kLaneCap;
-    const unsigned long long pk = cur[icur];
+    unsigned int* const snx = segs + (sgb ^ kLaneSeg);
+    // the next box of this level: its word is loaded now, used next iteration
+    const bool more = k + 1 < ncur;
+    const bool n_newseg = ilv && seg_k + 1 == 2 * seg_m;
+    const int n_start = n_newseg ? seg_start + 2 * seg_m : seg_start;
+    const int n_m = n_newseg ? seg_mn : seg_m;
+    const int n_k = n_newseg ? 0 : seg_k + 1;
+    const int n_i = seg_i + (n_newseg ? 1 : 0);
+    const int pos1 = !ilv ? k + 1 : (n_k < n_m ? n_start + 2 * n_k : n_start + 2 * (n_k - n_m) + 1);
+    if (more) pk_next = cur[pos1];
     const int suv = nu + nv;
     const unsigned long long ti = pk >> suv;
-    if (sd == 0) {
-      // t-split level: a new run of equal t_lo starts; the previous run's
-      // upper children follow its lower children
-      if (ti != run) {
-        for (int j = 0; j < ntmp; ++j) nxt[nn + j] = tmp[j];
-        nn += ntmp;
-        ntmp = 0;
-        run = ti;
-      }
-    }
+    // a t-split level: a new run of equal t_lo closes the previous run's
+    // segment of the next level
+    const bool new_run = sd == 0 && ti != run;
+    const bool close_run = new_run && run_m > 0;
+    if (close_run) snx[nsn] = (unsigned)run_m;
+    seg0 = close_run && nsn == 0 ? run_m : seg0;
+    nsn += close_run ? 1 : 0;
+    run_m = new_run ? 0 : run_m;
+    run = sd == 0 ? ti : run;
     Box b;
     b.t0 = (double)ti * wt; b.t1 = b.t0 + wt;
     b.u0 = (double)((pk >> nv) & ((1ull << nu) - 1ull)) * wu; b.u1 = b.u0 + wu;
     b.v0 = (double)(pk & ((1ull << nv) - 1ull)) * wv; b.v1 = b.v0 + wv;
     double wb;
-    const int cls = classify_k<KIND, true>(P, b, eps, sep, wb);
+    const int cls = classify_full<KIND>(P, b, eps, sep, wb);
     ++C;
-    ++st[KIND];
+    ++st.cls;
+    const bool disj = cls == kDisjoint;
+    const bool budget = C >= mc;
+    const bool accept = !disj && (wb < delta || cls == kContained);  // (:215)
+    // first colliding box of this level (:201-206)
+    const int shape = nt | (nu << 8) | (nv << 16);
+    const bool first = !disj && !col_lvl;
+    fr.pk = first ? pk : fr.pk;
+    fr.shape = first ? shape : fr.shape;
+    fr.level = first ? L : fr.level;
+    fr.codom = first ? wb : fr.codom;
+    fr.t0 = first ? b.t0 : fr.t0;
+    hf = hf || first;
+    // the ways this box can end the query
+    const bool end_disj = disj && budget && (hd || more || nn > 0);   // (:188-199)
+    const bool end_budget = !disj && budget;                          // (:208-213)
+    const bool end_acc = accept && !budget && !col_lvl;               // (:243-252)
     int outcome = 0;  // 0 continue, 1 ended (result written), 2 evict
-    if (cls == kDisjoint) {
-      // budget with boxes outstanding: the earliest record (_kernel.py:188-199)
-      if (C >= mc && (hd || icur + 1 < ncur || nn + ntmp > 0)) {
-        lane_write(a, q, hd && (!hf || dr.t0 < fr.t0), dr, fr, t_max, C, 1);
-        outcome = 1;
-      }
-    } else {
-      const LaneRecBox me{pk, nt | (nu << 8) | (nv << 16), L, wb, b.t0};
-      if (!col) { fr = me; hf = true; }  // first colliding box of this level (:201-206)
-      if (C >= mc) {                     // budget (:208-213)
-        lane_write(a, q, hd && dr.t0 < fr.t0, dr, fr, t_max, C, 1);
-        outcome = 1;
-      } else if (wb < delta || cls == kContained) {  // accept (:215, 243-258)
-        if (!col) {
-          lane_write(a, q, hd && dr.t0 < b.t0, dr, me, t_max, C, 0);
-          outcome = 1;
-        } else if (!hd || b.t0 < dr.t0) {
-          dr = me;
-          hd = true;
-        }
-      } else if (nn + ntmp + 2 > kLaneCap) {
-        outcome = 2;  // the next level outgrows this tier
-      } else {
-        // refine along the level's split dimension: insert the child bit
-        const int pos = sd == 0 ? suv : (sd == 1 ? nv : 0);
-        const unsigned long long lo = ((pk >> pos) << (pos + 1)) | (pk & ((1ull << pos) - 1ull));
-        const unsigned long long hi = lo | (1ull << pos);
-        if (sd == 0) {
-          nxt[nn++] = lo;
-          tmp[ntmp++] = hi;
-        } else {
-          nxt[nn++] = lo;
-          // vertex-face: the upper child of a u / v split only inside u + v <= 1
-          // (_kernel.py:276-310)
-          bool push_hi = true;
-          if (KIND == 0) {
-            if (sd == 1) push_hi = 0.5 * (b.u0 + b.u1) + b.v0 <= 1.0;
-            else push_hi = b.u0 + 0.5 * (b.v0 + b.v1) <= 1.0;
-          }
-          if (push_hi) nxt[nn++] = hi;
-        }
-      }
-      col = true;
+    if (end_disj || end_budget || end_acc) {
+      const LaneRecBox me{pk, shape, L, wb, b.t0};
+      const bool use_drop = hd && (end_acc ? dr.t0 < b.t0
+                                           : (end_disj ? (!hf || dr.t0 < fr.t0) : dr.t0 < fr.t0));
+      lane_write(a, q, use_drop, dr, end_acc ? me : fr, t_max, C, end_acc ? 0 : 1);
+      outcome = 1;
     }
-    if (outcome == 0 && ++icur == ncur) {
-      // ---- level end
-      for (int j = 0; j < ntmp; ++j) nxt[nn + j] = tmp[j];
-      nn += ntmp;
-      ntmp = 0;
-      if (nn == 0) {
-        // queue exhausted (_kernel.py:321-324)
-        if (hd) {
-          lane_write(a, q, true, dr, dr, t_max, C, 0);
-        } else {
-          const Box z = {0, 0, 0, 0, 0, 0};
-          write_result(a, q, kFree, z, 0.0, C, 0, 0);
-        }
-        outcome = 1;
-      } else {
-        cb ^= kLaneCap;
-        ncur = nn;
-        nn = 0;
-        icur = 0;
-        ++L;
-        col = false;
-        run = ~0ull;
-        // every refining box of the level split along sd
-        int ns;
-        if (sd == 0) { ns = ++nt; wt *= 0.5; }
-        else if (sd == 1) { ns = ++nu; wu *= 0.5; }
-        else { ns = ++nv; wv *= 0.5; }
-        if (ns > kLaneMaxSplits || L > kLaneMaxLevel) outcome = 2;
-        sd = lane_split_dim(wt, wu, wv, kap);
-      }
+    // an accepted box after the level's first: the drop record (:253-258)
+    const bool drop = accept && !budget && col_lvl && (!hd || b.t0 < dr.t0);
+    dr.pk = drop ? pk : dr.pk;
+    dr.shape = drop ? shape : dr.shape;
+    dr.level = drop ? L : dr.level;
+    dr.codom = drop ? wb : dr.codom;
+    dr.t0 = drop ? b.t0 : dr.t0;
+    hd = hd || drop;
+    // refine along the level's split dimension: insert the child bit; the
+    // children are stored in push order.  Vertex-face: the upper child of a
+    // u / v split only inside u + v <= 1 (_kernel.py:276-310); t-split
+    // children are never clipped.
+    const bool refine = !disj && !budget && !accept;
+    const bool evict = refine && nn + 2 > kLaneCap;
+    const bool push = refine && !evict;
+    const int pos = sd == 0 ? suv : (sd == 1 ? nv : 0);
+    const unsigned long long lo = ((pk >> pos) << (pos + 1)) | (pk & ((1ull << pos) - 1ull));
+    const unsigned long long hi = lo | (1ull << pos);
+    bool push_hi = true;
+    if (KIND == 0) {
+      const bool hu = 0.5 * (b.u0 + b.u1) + b.v0 <= 1.0;
+      const bool hv = b.u0 + 0.5 * (b.v0 + b.v1) <= 1.0;
+      push_hi = sd == 0 ? true : (sd == 1 ? hu : hv);
     }
+    if (push) {
+      nxt[nn] = lo;
+      if (push_hi) nxt[nn + 1] = hi;
+    }
+    nxt0 = push && nn == 0 ? lo : nxt0;
+    nn += push ? (push_hi ? 2 : 1) : 0;
+    run_m += push && sd == 0 ? 1 : 0;
+    col_lvl = col_lvl || !disj;
+    outcome = evict ? 2 : outcome;
+    // advance to the next box
+    const bool go = outcome == 0;
+    k += go ? 1 : 0;
+    seg_start = go ? n_start : seg_start;
+    seg_m = go ? n_m : seg_m;
+    seg_k = go ? n_k : seg_k;
+    seg_i = go ? n_i : seg_i;
+    if (go && n_newseg && seg_i + 1 < nseg) seg_mn = (int)segs[sgb + seg_i + 1];
+    pk = go ? pk_next : pk;
+    // ---- level end
+    const bool lvl_end = go && k == ncur;
+    const bool close_last = lvl_end && run_m > 0;
+    if (close_last) snx[nsn] = (unsigned)run_m;
+    seg0 = close_last && nsn == 0 ? run_m : seg0;
+    nsn += close_last ? 1 : 0;
+    run_m = lvl_end ? 0 : run_m;
+    if (lvl_end && nn == 0) {
+      // queue exhausted (_kernel.py:321-324)
+      if (hd) {
+        lane_write(a, q, true, dr, dr, t_max, C, 0);
+      } else {
+        const Box z = {0, 0, 0, 0, 0, 0};
+        write_result(a, q, kFree, z, 0.0, C, 0, 0);
+      }
+      outcome = 1;
+    }
+    const bool nl = lvl_end && nn > 0;  // the next level becomes current
+    cb = nl ? cb ^ kLaneCap : cb;
+    sgb = nl ? sgb ^ kLaneSeg : sgb;
+    const bool nilv = sd == 0;
+    if (nl && nilv && nsn > 1) seg_mn = (int)segs[sgb + 1];
+    ilv = nl ? nilv : ilv;
+    nseg = nl ? nsn : nseg;
+    seg_start = nl ? 0 : seg_start;
+    seg_k = nl ? 0 : seg_k;
+    seg_i = nl ? 0 : seg_i;
+    seg_m = nl ? seg0 : seg_m;
+    ncur = nl ? nn : ncur;
+    k = nl ? 0 : k;
+    pk = nl ? nxt0 : pk;
+    nn = nl ? 0 : nn;
+    nsn = nl ? 0 : nsn;
+    run = nl ? ~0ull : run;
+    L += nl ? 1 : 0;
+    col_lvl = nl ? false : col_lvl;
+    // every refining box of the level split along sd
+    const bool st_ = nl && sd == 0, su_ = nl && sd == 1, sv_ = nl && sd == 2;
+    nt += st_ ? 1 : 0; wt = st_ ? 0.5 * wt : wt;
+    nu += su_ ? 1 : 0; wu = su_ ? 0.5 * wu : wu;
+    nv += sv_ ? 1 : 0; wv = sv_ ? 0.5 * wv : wv;
+    const int ns = sd == 0 ? nt : (sd == 1 ? nu : nv);
+    outcome = nl && (ns > kLaneMaxSplits || L > kLaneMaxLevel) ? 2 : outcome;
+    sd = nl ? lane_split_dim(wt, wu, wv, kapr) : sd;
     if (outcome == 1) {
-      st[2 + KIND] += (unsigned long long)(C - 1);  // checks of finished queries (root: prologue's)
-      st[4 + KIND] += 1;
-      active = false;
+      st.checks += (unsigned long long)(C - 1);  // checks of finished queries (root: prologue's)
+      st.done += 1;
+      state = 0;
     } else if (outcome == 2) {
       // restart from the root in the light tier (one self-contained record)
       const unsigned long long h = atomicAdd(io.out_count, 1ull);
-      Pre& p = io.out[h];
-      for (int k = 0; k < 24; ++k) p.P[k] = P[k];
-      QueryParams qp;
-      qp.eps[0] = eps[0]; qp.eps[1] = eps[1]; qp.eps[2] = eps[2];
-      qp.kap[0] = kap[0]; qp.kap[1] = kap[1]; qp.kap[2] = kap[2];
-      qp.sep = sep; qp.delta = delta; qp.t_max = t_max; qp.max_checks = mc;
-      qp.kind = KIND; qp.tame = 1;
-      p.qp = qp;
-      p.q = q;
-      p.wb = 0.0;
-      p.flag = 0;
-      p.pad = 0;
-      st[6] += 1;
-      st[7] += (unsigned long long)(C - 1);  // lane checks that the light tier repeats
-      active = false;
+      io.out[h] = Pre{q, 0.0, 0u, 0u};
+      st.evicted += 1;
+      st.wasted += (unsigned long long)(C - 1);  // lane checks that the light tier repeats
+      state = 0;
     }
   }
 }
 
 __global__ void __launch_bounds__(kLaneNT, TCCD_NMINB) lane_kernel(Args a, LaneIO io) {
-  __shared__ double Ps[24 * kLaneNT];
+  __shared__ double Ps[kLaneCol * kLaneNT];
   const long long gt = (long long)blockIdx.x * kLaneNT + threadIdx.x;
-  unsigned long long* lb = io.scratch + gt * 3 * kLaneCap;
-  double* colbase = Ps + threadIdx.x;
+  unsigned long long* lb = io.scratch + gt * kLaneScratchWords;
+  double* col = Ps + threadIdx.x;
   const unsigned long long nvf = io.count[0], nee = io.count[1];
   // first kind of this warp: warps split between the kinds in proportion to
   // their queues; a warp whose queue runs dry moves to the other one
   const long long gw = gt >> 5, nw = (long long)gridDim.x * (kLaneNT / 32);
   int kind = (nvf + nee) > 0 && (unsigned long long)gw * (nvf + nee) < nee * (unsigned long long)nw;
-  unsigned long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  LaneStats s0, s1;
   for (int pass = 0; pass < 2; ++pass, kind ^= 1) {
-    if (kind == 0) lane_loop<0>(a, io, colbase, lb, st);
-    else lane_loop<1>(a, io, colbase, lb, st);
+    if (kind == 0) lane_loop<0>(a, io, col, lb, s0);
+    else lane_loop<1>(a, io, col, lb, s1);
   }
+  const unsigned long long v[8] = {s0.cls, s1.cls, s0.checks, s1.checks, s0.done, s1.done,
+                                   s0.evicted + s1.evicted, s0.wasted + s1.wasted};
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    unsigned long long v = st[k];
+  for (int i = 0; i < 8; ++i) {
+    unsigned long long x = v[i];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&io.stats[k], v);
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&io.stats[i], x);
   }
 }
 

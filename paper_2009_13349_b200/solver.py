@@ -161,7 +161,7 @@ def _param(x, n, dtype, device, name):
     return t.to(device=device, dtype=dtype, non_blocking=True).contiguous(), 0
 
 
-CHUNK = 1 << 22  # queries per library chunk (csrc/tccd.cu kChunk)
+CHUNK = 1 << 22  # queries per host-copy piece (non_blocking host inputs)
 
 
 def _params(kind, config, delta, max_checks, separation, t_max, n, dev):
@@ -217,11 +217,12 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
     raised (check status after synchronizing).
 
     stats=True adds out["stats"], the library's diagnostic counters
-    (TCCD_STAT_*, include/tccd.h).  events: optional len(STAGES)
-    torch.cuda.Event(enable_timing=True), recorded on the launching stream
-    after the prologue, lane, light, medium and giant stages (per-kernel
-    timing).  info: an optional dict that receives "launches", the number of
-    kernels the call launched.
+    (TCCD_STAT_*, include/tccd.h).  events: optional list of
+    torch.cuda.Event(enable_timing=True); the library records one on the
+    launching stream after each stage launch, in order, and
+    info["event_stages"] names each recorded one's stage (an index into
+    STAGES): per-kernel timing (see stage_times).  info: an optional dict
+    that also receives "launches", the number of kernels the call launched.
 
     hits=True adds the compacted hit list: out["hit_index"] (int64) and
     out["hit_toi"] (float64), one entry per query with status 1 in no
@@ -253,10 +254,10 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
     if host_in and non_blocking:
         # every host input goes over on the API's copy stream: an engine copy
         # issued on the launching stream would queue behind the solve already
-        # there and hold back the next call's copies.  A batch of several
-        # library chunks is copied chunk by chunk, each chunk's solve waiting
-        # only for its own points, so the copy overlaps the solve inside one
-        # call as well.
+        # there and hold back the next call's copies.  A large batch is copied
+        # in pieces of CHUNK queries, each piece's prologue waiting (inside
+        # the library) only for its own points, so the copy overlaps the solve
+        # inside one call as well.
         compute = torch.cuda.current_stream(dev)
         cs = copy_stream(dev)
         slot = _staging_buffer(dev, pts.numel() * 8)
@@ -264,7 +265,7 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
             dst = slot[0][:pts.numel() * 8].view(torch.float64).view(pts.shape)
             kind_t, kind_all, delta_t, delta_all, mc_t, mc_all, sep_t, sep_all, tm_t, tm_all, \
                 mc_src, sep_src = _params(kind, config, delta, max_checks, separation, t_max, n, dev)
-            if n > CHUNK and stats is False and events is None:
+            if n > CHUNK:
                 chunk_events = []
                 for lo in range(0, n, CHUNK):
                     dst[lo:lo + CHUNK].copy_(pts[lo:lo + CHUNK], non_blocking=True)
@@ -328,14 +329,16 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
         out["hit_toi"] = torch.empty(n, dtype=torch.float64, device=dev)
         out["hit_count"] = torch.zeros(1, dtype=torch.int64, device=dev)
     st = torch.zeros(_lib.NUM_STATS, dtype=torch.int64, device=dev) if stats else None
-    ev_arr = None
+    ev_arr = stage_arr = None
     if events is not None:
-        if len(events) != len(STAGES):
-            raise ValueError(f"events must hold {len(STAGES)} torch.cuda.Event")
         for ev in events:
             if ev.cuda_event == 0:  # torch creates the handle on first record
                 ev.record(torch.cuda.current_stream(dev))
-        ev_arr = (ctypes.c_void_p * len(STAGES))(*[ev.cuda_event for ev in events])
+        ev_arr = (ctypes.c_void_p * len(events))(*[ev.cuda_event for ev in events])
+        stage_arr = (ctypes.c_int32 * len(events))()
+    in_arr = None
+    if chunk_events is not None:
+        in_arr = (ctypes.c_void_p * len(chunk_events))(*[ev.cuda_event for ev in chunk_events])
     flags = (_lib.FLAG_HEAVY_ONLY if heavy_only else 0) | (0 if lanes else _lib.FLAG_NO_LANE)
     n_launch = [0]
 
@@ -349,7 +352,7 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
         def sl(t, lo, hi):
             return None if t is None else t[lo:hi]
 
-        def launch(lo, hi, ev_arr=None):
+        def launch(lo, hi):
             b = _lib.TccdBatch()
             b.struct_size = ctypes.sizeof(_lib.TccdBatch)
             b.flags = flags
@@ -374,7 +377,14 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
             b.heavy_blocks = hb
             b.device_sms = sm_count(dev)
             b.stats = _ptr(st)
-            b.events = ctypes.cast(ev_arr, ctypes.c_void_p) if ev_arr is not None else None
+            if ev_arr is not None:
+                b.events = ctypes.cast(ev_arr, ctypes.c_void_p)
+                b.event_stage = ctypes.cast(stage_arr, ctypes.c_void_p)
+                b.n_events = len(events)
+            if in_arr is not None:
+                b.input_events = ctypes.cast(in_arr, ctypes.c_void_p)
+                b.input_chunk = CHUNK
+                b.n_input_events = len(chunk_events)
             if hits:
                 b.hit_index = _ptr(out["hit_index"])
                 b.hit_toi = _ptr(out["hit_toi"])
@@ -384,14 +394,11 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
             b.pool_boxes = int(pool_boxes)
             rc = lib.tccd_solve_batch(ctypes.byref(b), ctypes.c_void_p(stream.cuda_stream))
             n_launch[0] += int(b.launches)
+            if ev_arr is not None and info is not None:
+                info["event_stages"] = [int(stage_arr[i]) for i in range(b.events_used)]
             _raise_abi(rc, delta_all, mc_all, tm_all, sep_all, kind_all)
 
-        if chunk_events is None:
-            launch(0, n, ev_arr)
-        else:
-            for c, ev in enumerate(chunk_events):
-                stream.wait_event(ev)
-                launch(c * CHUNK, min(n, (c + 1) * CHUNK))
+        launch(0, n)
         _workspace_release(dev, stream)
     if host_in and non_blocking:
         # results into pinned host tensors by a copy kernel on the launching
@@ -458,6 +465,19 @@ def solve_batch(points, kind, config: SolverConfig | None = None, *, delta=None,
         info["launches"] = n_launch[0]
     if raise_on_error and n and "status" in out:
         _raise_status(out["status"])
+    return out
+
+
+def stage_times(start, events, stages) -> dict:
+    """Milliseconds per stage from a start event recorded before a
+    solve_batch call and its events / info["event_stages"] (each recorded
+    event closes the stage it names; the gap from the previous event is that
+    stage's time)."""
+    out = {nm: 0.0 for nm in STAGES}
+    prev = start
+    for ev, sg in zip(events, stages):
+        out[STAGES[sg]] += prev.elapsed_time(ev)
+        prev = ev
     return out
 
 

@@ -21,6 +21,7 @@ ap.add_argument("--sep", type=float, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--heavy-only", action="store_true")
 ap.add_argument("--heavy-blocks", type=int, default=None)
+ap.add_argument("--no-lanes", action="store_true")
 args = ap.parse_args()
 w = W.generate(args.config, args.start, args.queries, separation=args.sep)
 dev = torch.device("cuda", 0)
@@ -29,19 +30,23 @@ kind = torch.from_numpy(w.kind).to(dev)
 kw = {}
 if args.config == 2:
     kw = dict(delta=torch.from_numpy(w.delta).to(dev), max_checks=torch.from_numpy(w.max_checks).to(dev))
+from paper_2009_13349_b200 import _lib, solver  # noqa: E402
 for r in range(args.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(solver.STAGES))]
     e0.record()
     out = solve_batch(pts, kind, outputs=("status", "toi", "checks"), device=dev,
                       separation=w.separation, heavy_only=args.heavy_only, stats=True,
-                      heavy_blocks=args.heavy_blocks,
-                      events=ev, **kw)
+                      heavy_blocks=args.heavy_blocks, lanes=not args.no_lanes,
+                      events=ev if args.queries <= solver.CHUNK else None, **kw)
     e1.record()
     torch.cuda.synchronize()
     st = out["stats"].tolist()
-    stages = [e0.elapsed_time(ev[0])] + [ev[j].elapsed_time(ev[j + 1]) for j in range(3)]
-    print(f"rep {r}: {e0.elapsed_time(e1):.2f} ms  stages " + "/".join(f"{x:.2f}" for x in stages) +
-          f"  checks {int(out['checks'].sum())} "
-          f"giant {st[0]} medium {st[3]} rounds {st[1]} deferrals {st[2]} "
-          f"boxes L/M/G {st[4]}/{st[5]}/{st[6]}", flush=True)
+    stages = ""
+    if args.queries <= solver.CHUNK:
+        t = [e0.elapsed_time(ev[0])] + [ev[j].elapsed_time(ev[j + 1]) for j in range(len(ev) - 1)]
+        stages = " stages " + "/".join(f"{nm} {x:.2f}" for nm, x in zip(solver.STAGES, t))
+    print(f"rep {r}: {e0.elapsed_time(e1):.2f} ms{stages}  checks {int(out['checks'].sum())} "
+          f"lane q {st[_lib.STAT_LANE_QUERIES]} evicted {st[_lib.STAT_LANE_EVICTED]} "
+          f"giant {st[_lib.STAT_GIANT_QUERIES]} medium {st[_lib.STAT_MEDIUM_QUERIES]} "
+          f"rounds {st[_lib.STAT_ROUNDS]} deferrals {st[_lib.STAT_DEFERRALS]}", flush=True)
