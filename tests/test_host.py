@@ -232,7 +232,8 @@ def test_workspace_scales_with_the_batch():
     assert one < 400e6
     small = L.tccd_workspace_bytes(1, 1000, 1)
     assert small < 20e6
-    sizes = [L.tccd_workspace_bytes(n, 1000, 1) for n in (1, 10, 1000, 100_000, 1 << 22, 1 << 23)]
+    sizes = [L.tccd_workspace_bytes(n, 1000, 1) for n in (1, 10, 1000, 100_000, 1 << 22, 1 << 26,
+                                                          1 << 27)]
     assert all(a <= b for a, b in zip(sizes, sizes[1:]))
     assert sizes[-1] == sizes[-2]  # bounded by one library chunk
     # the handover pool size is a parameter; a smaller pool never grows the layout
