@@ -282,6 +282,23 @@ int tccd_copy_to_host(const void *src, void *host_dst, int64_t bytes, void *stre
 
 void tccd_release_cached(void);
 
+/*
+ * The reference's spec-level inclusion functions, batched, on the device
+ * (the solver's own arithmetic; the solver does not call them).  DEVICE
+ * pointers; kind NULL -> kind_all; asynchronous on `stream`.
+ *   tccd_box_hulls <- ccdkit.inclusion.box_inclusion (inclusion.py:131-156):
+ *       for each i, lo[i][ax] / hi[i][ax] = min / max over the 8 corners of
+ *       boxes[i] = (t0, t1, u0, u1, v0, v1) of axis ax of F (NaN if a corner
+ *       value is NaN, as numpy's min / max).
+ *   tccd_kappas <- ccdkit.inclusion.kappas (inclusion.py:195-217) =
+ *       ccdkit._kernel._kappas (_kernel.py:98-132): out[i] = (k_t, k_u, k_v)
+ *       on [0, t_max] x [0,1]^2 (t_max NULL -> t_max_all).
+ */
+int tccd_box_hulls(const double *points, const uint8_t *kind, int kind_all, const double *boxes,
+                   int64_t n, double *lo, double *hi, void *stream);
+int tccd_kappas(const double *points, const uint8_t *kind, int kind_all, const double *t_max,
+                double t_max_all, int64_t n, double *out, void *stream);
+
 /* Copy the first min(*count, max_elems) elements of elem_bytes each from
  * device array src to pinned host memory, where *count (device) was written
  * by an earlier kernel on `stream` (a compacted hit list, tccd_batch.

@@ -130,6 +130,8 @@ EXPORTS = (
     "tccd_copy_to_host",
     "tccd_copy_counted_to_host",
     "tccd_release_cached",
+    "tccd_box_hulls",
+    "tccd_kappas",
     "tccd_irf_workspace_bytes",
     "tccd_irf_batch",
 )
@@ -162,6 +164,11 @@ def lib() -> ctypes.CDLL:
                                               ctypes.c_int64]
         L.tccd_release_cached.restype = None
         L.tccd_release_cached.argtypes = []
+        L.tccd_box_hulls.restype = ctypes.c_int
+        L.tccd_box_hulls.argtypes = [_vp, _vp, ctypes.c_int, _vp, ctypes.c_int64, _vp, _vp, _vp]
+        L.tccd_kappas.restype = ctypes.c_int
+        L.tccd_kappas.argtypes = [_vp, _vp, ctypes.c_int, _vp, ctypes.c_double, ctypes.c_int64,
+                                  _vp, _vp]
         L.tccd_solve_batch.restype = ctypes.c_int
         L.tccd_solve_batch.argtypes = [ctypes.POINTER(TccdBatch), _vp]
         L.tccd_solve_kernel.restype = ctypes.c_int

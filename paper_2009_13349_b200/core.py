@@ -1,10 +1,11 @@
 """Host-side types mirroring the reference's solve-side API.
 
 Same names, fields, validation rules and exception classes as
-pkg/src/ccdkit/core.py (QueryKind :75-79, Query :83-116, DomainBox :120-150,
-SolverConfig :154-184, CCDResult :188-209), so reference callers switch by
-changing the import.  The numerics live on the GPU (csrc/); nothing here
-evaluates F.
+pkg/src/ccdkit/core.py (Vec3 :42-72, QueryKind :75-79, Query :83-116,
+DomainBox :120-150, SolverConfig :154-184, CCDResult :188-209), so
+reference callers switch by changing the import.  The solver's numerics live
+on the GPU (csrc/); the scalar ``eval_F*`` here are the reference's
+point-wise definition of F (core.py:225-256), for callers and tests.
 """
 
 from __future__ import annotations
@@ -12,6 +13,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 from enum import IntEnum
+from typing import NamedTuple
 
 import numpy as np
 
@@ -23,13 +25,49 @@ class QueryKind(IntEnum):
     EDGE_EDGE = 1
 
 
-def _vec3(p) -> tuple[float, float, float]:
+class _XYZ(NamedTuple):
+    x: float
+    y: float
+    z: float
+
+
+class Vec3(_XYZ):
+    """Three finite binary64 components (core.py:42-72): a tuple, with the
+    reference's component-wise arithmetic."""
+
+    __slots__ = ()
+
+    def __new__(cls, x, y, z):
+        c = (float(x), float(y), float(z))
+        if not all(math.isfinite(v) for v in c):
+            raise ValueError(f"Vec3 components must be finite, got {c}")
+        return tuple.__new__(cls, c)
+
+    @classmethod
+    def _trusted(cls, x: float, y: float, z: float) -> "Vec3":
+        return tuple.__new__(cls, (x, y, z))
+
+    def __add__(self, o):
+        return Vec3(self[0] + o[0], self[1] + o[1], self[2] + o[2])
+
+    def __sub__(self, o):
+        return Vec3(self[0] - o[0], self[1] - o[1], self[2] - o[2])
+
+    def scaled(self, s: float) -> "Vec3":
+        return Vec3(self[0] * s, self[1] * s, self[2] * s)
+
+    def dot(self, o) -> float:
+        return self[0] * o[0] + self[1] * o[1] + self[2] * o[2]
+
+    def cross(self, o) -> "Vec3":
+        return Vec3(self[1] * o[2] - self[2] * o[1], self[2] * o[0] - self[0] * o[2],
+                    self[0] * o[1] - self[1] * o[0])
+
+
+def _vec3(p) -> Vec3:
     if len(p) != 3:
         raise ValueError(f"a point needs 3 coordinates, got {len(p)}")
-    x, y, z = (float(c) for c in p)
-    if not (math.isfinite(x) and math.isfinite(y) and math.isfinite(z)):
-        raise ValueError(f"Vec3 components must be finite, got ({x}, {y}, {z})")
-    return (x, y, z)
+    return p if type(p) is Vec3 else Vec3(*p)
 
 
 @dataclass(frozen=True)
@@ -58,8 +96,8 @@ class Query:
         without re-validating 24 coordinates one by one."""
         q = object.__new__(cls)
         q.__dict__["kind"] = kind
-        q.__dict__["points0"] = points0
-        q.__dict__["points1"] = points1
+        q.__dict__["points0"] = tuple(Vec3._trusted(*p) for p in points0)
+        q.__dict__["points1"] = tuple(Vec3._trusted(*p) for p in points1)
         return q
 
     def as_arrays(self) -> tuple[np.ndarray, np.ndarray]:
@@ -141,3 +179,32 @@ class CCDResult:
     @property
     def colliding(self) -> bool:
         return self.toi is not None
+
+
+# --------------------------------------------------------------------------
+# F(t, u, v) at one point, the reference's scalar definition (core.py:
+# 221-256): each point lerped to t as (1 - t) * start + t * end, then
+#   VF: p - ((1 - u - v) * v1 + u * v2 + v * v3)
+#   EE: ((1 - u) * p1 + u * p2) - ((1 - v) * p3 + v * p4)
+# in binary64, left to right.  The device hull (csrc/tccd_device.cuh) is
+# bit-identical to these at every corner (tests/test_gpu_api.py).
+
+
+def _at(q: Query, t: float):
+    omt = 1.0 - t
+    return [tuple(omt * a[i] + t * b[i] for i in range(3)) for a, b in zip(q.points0, q.points1)]
+
+
+def eval_F_vf(q: Query, t: float, u: float, v: float) -> Vec3:
+    p, a, b, c = _at(q, t)
+    w = 1.0 - u - v
+    return Vec3(*(p[i] - (w * a[i] + u * b[i] + v * c[i]) for i in range(3)))
+
+
+def eval_F_ee(q: Query, t: float, u: float, v: float) -> Vec3:
+    a, b, c, d = _at(q, t)
+    return Vec3(*(((1.0 - u) * a[i] + u * b[i]) - ((1.0 - v) * c[i] + v * d[i]) for i in range(3)))
+
+
+def eval_F(q: Query, t: float, u: float, v: float) -> Vec3:
+    return eval_F_vf(q, t, u, v) if q.kind == QueryKind.VERTEX_FACE else eval_F_ee(q, t, u, v)

@@ -567,3 +567,47 @@ def warm_up(device=None) -> None:
     pts = torch.from_numpy(vf.all_coordinates()).reshape(1, 8, 3)
     solve_batch(pts, 0, SolverConfig(max_checks=16), device=device)
     solve_batch(pts, 0, SolverConfig(max_checks=16), device=device, heavy_only=True)
+
+
+# --------------------------------------------------------------------------
+# The solver's traversal rules at the level of one DomainBox (solver.py:
+# 110-172 of the reference), for callers and tests.  The device engine
+# applies the same rules to whole levels (csrc/tccd_engine.cuh,
+# csrc/tccd_lane.cuh).
+
+
+def split(box: DomainBox, kappa, kind: QueryKind) -> tuple:
+    """Bisect ``box`` along the dimension whose width x kappa is largest
+    (strictly: ties go to t, then u, then v) at 0.5 * (lo + hi); a vertex-face
+    child with u_lo + v_lo > 1 (outside the triangle) is dropped.  Raises
+    ValueError when every weighted width is 0 (F is constant on the box)."""
+    kt, ku, kv = (float(k) for k in kappa)
+    if kt < 0.0 or ku < 0.0 or kv < 0.0:
+        raise ValueError("kappa components must be >= 0")
+    c = ((box.t[1] - box.t[0]) * kt, (box.u[1] - box.u[0]) * ku, (box.v[1] - box.v[0]) * kv)
+    dim = 0
+    if c[1] > c[dim]:
+        dim = 1
+    if c[2] > c[dim]:
+        dim = 2
+    if c[dim] <= 0.0:
+        raise ValueError("box has no splittable dimension (F constant over it)")
+    iv = [box.t, box.u, box.v]
+    lo, hi = iv[dim]
+    mid = 0.5 * (lo + hi)
+    kids = []
+    for half in ((lo, mid), (mid, hi)):
+        parts = list(iv)
+        parts[dim] = half
+        kids.append(DomainBox(parts[0], parts[1], parts[2], box.level + 1))
+    if kind == QueryKind.VERTEX_FACE:
+        kids = [k for k in kids if k.u[0] + k.v[0] <= 1.0]
+    return tuple(kids)
+
+
+def queue_order(a: DomainBox, b: DomainBox) -> int:
+    """-1 / 0 / 1 as ``a`` is visited before / together with / after ``b``:
+    by level, then by t_lo (equal keys keep push order: the queue's sort is
+    stable)."""
+    ka, kb = (a.level, a.t[0]), (b.level, b.t[0])
+    return -1 if ka < kb else (1 if ka > kb else 0)

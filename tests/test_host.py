@@ -247,3 +247,18 @@ def test_solve_batch_fails_loudly_without_gpu():
     from paper_2009_13349_b200 import solve_batch
     with pytest.raises(RuntimeError):
         solve_batch(np.zeros((1, 8, 3)), 0, device="cpu")
+
+
+def test_bench_launcher_starts_n_ranks():
+    """`bench.py --gpus 2` re-launches itself under torch.distributed.run with
+    two ranks (here: the CPU launcher self-test, gloo, no solve); the line
+    reports n_gpus 2 and the two contiguous shards of the one query set."""
+    import json
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--selftest-launcher", "--queries", "1001"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["shards"] == [[0, 500], [500, 1001]]

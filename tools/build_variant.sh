@@ -7,4 +7,4 @@ ROOT="$(cd "$(dirname "$0")/.." && pwd)"
 name="$1"; shift
 cd "$ROOT/paper_2009_13349_b200/csrc"
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-  -I"$ROOT/include" --fmad=false "$@" -shared -o "$ROOT/exp/lib_${name}.so" tccd.cu broad.cu irf.cu
+  -I"$ROOT/include" --fmad=false "$@" -shared -o "$ROOT/exp/lib_${name}.so" tccd.cu broad.cu irf.cu mirror.cu
