@@ -87,14 +87,16 @@ extern "C" {
                                        tier and kind (light VF, light EE, medium
                                        VF, medium EE, giant VF, giant EE)       */
 #define TCCD_STAT_LANE_CLS 14       /* [14..15] lane classifications VF, EE     */
-#define TCCD_STAT_LANE_CHECKS 16    /* [16..17] checks of the queries the lane
-                                       tier finished, root check excluded (the
-                                       prologue's): the reference's own count,
-                                       so algorithmic work                      */
+#define TCCD_STAT_LANE_CHECKS 16    /* [16..17] checks the lane tier did on the
+                                       reference's path (queries it finished or
+                                       handed over with their level; root check
+                                       excluded: the prologue's): algorithmic
+                                       work                                     */
 #define TCCD_STAT_LANE_DONE 18      /* [18..19] queries the lane tier finished  */
 #define TCCD_STAT_LANE_EVICTED 20   /* queries the lane tier sent to the light
-                                       tier (restart from the root)             */
-#define TCCD_STAT_LANE_WASTED 21    /* lane checks of those queries             */
+                                       tier (handed over or restarting)         */
+#define TCCD_STAT_LANE_WASTED 21    /* lane checks of those that restart (the
+                                       light tier repeats them)                 */
 #define TCCD_STAT_POOL_DEMAND 22    /* [22..23] handover boxes requested light->
                                        medium, medium->giant                    */
 #define TCCD_STAT_RESTARTS 24       /* [24..25] evictions light->medium,
@@ -106,7 +108,9 @@ extern "C" {
                                        point, deferral re-runs and restarted
                                        work excluded)                           */
 #define TCCD_STAT_PROLOGUE_DONE 29  /* queries decided at the root (or invalid) */
-#define TCCD_STAT_CHUNKS 31         /* library chunks ([30] reserved)           */
+#define TCCD_STAT_LANE_HANDED 30    /* lane evictions handed over with their
+                                       current level (the rest restart)         */
+#define TCCD_STAT_CHUNKS 31         /* library chunks                           */
 
 /*
  * One batched solve.  All array pointers are DEVICE pointers.  For every

@@ -38,6 +38,7 @@ STAT_POOL_DEMAND = 22   # [22..23]
 STAT_RESTARTS = 24      # [24..25]
 STAT_TIER_CHECKS = 26   # [26..28]
 STAT_PROLOGUE_DONE = 29
+STAT_LANE_HANDED = 30
 STAT_CHUNKS = 31
 
 STATUS_FREE = 0

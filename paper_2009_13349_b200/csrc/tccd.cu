@@ -45,10 +45,14 @@ struct Counters {
   unsigned long long light_count;    // light-queue entries: prologue survivors + lane evictions
   unsigned long long lane_count[2];  // lane-tier queue entries per kind (VF, EE)
   unsigned long long lane_next[2];   // next lane entry to take per kind
-  // lane tier: [0..1] classifications VF / EE, [2..3] checks of the queries
-  // it finished (root check excluded: the prologue's), [4..5] queries
-  // finished, [6] queries evicted to the light tier, [7] their lane checks
-  unsigned long long lane[8];
+  // lane tier: [0..1] classifications VF / EE, [2..3] checks on the
+  // reference's path (queries it finished or handed over; root check
+  // excluded: the prologue's), [4..5] queries finished, [6] queries sent to
+  // the light tier, [7] lane checks of those that restart there, [8] of
+  // those, the ones handed over with their current level
+  unsigned long long lane[10];
+  unsigned long long lane_hand;      // lane-tier handover records used
+  unsigned long long lane_pool;      // lane-tier handover pool boxes used
   // ---- per group-tier sub-chunk (zeroed before each)
   unsigned long long q_count[3];  // entries in the medium / giant queues ([0] unused: light_count)
   unsigned long long q_next[3];   // next entry to admit (light: within the sub-chunk's slice)
@@ -69,7 +73,7 @@ struct Pre {
   long long q;         // query index
   double wb;           // root hull width (valid when flag says non-disjoint)
   unsigned int flag;   // root class flag (0: not classified yet)
-  unsigned int pad;
+  unsigned int pad;    // light queue: index of the lane tier's handover (~0: none)
 };
 static_assert(sizeof(Pre) == 24, "Pre layout");
 
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long
 #else
             pre.flag = make_flag(cls, acc, sdim, ph) | 64u;
 #endif
-            pre.pad = 0;
+            pre.pad = 0xffffffffu;
           }
         }
       }
@@ -410,6 +414,7 @@ __global__ void stats_kernel(Args a, int heavy_only, long long cnt, int batch, l
       }
       S[TCCD_STAT_LANE_EVICTED] += (long long)c.lane[6];
       S[TCCD_STAT_LANE_WASTED] += (long long)c.lane[7];
+      S[TCCD_STAT_LANE_HANDED] += (long long)c.lane[8];
       // survivors of the root check: the lane queue plus the prologue's
       // light-queue entries (the lane tier's evictions joined that queue)
       const unsigned long long into_light = c.light_count - c.lane[6];
@@ -525,9 +530,15 @@ int device_sm_count(int hint) {
 
 long long giant_cap(long long mcmax) { return 2 * mcmax + 2; }
 
+#ifndef TCCD_LANE_HAND
+#define TCCD_LANE_HAND (1LL << 21)
+#endif
+constexpr long long kLaneHandMax = TCCD_LANE_HAND;  // lane-tier handover records per chunk
+
 struct Layout {
   size_t ctr, light_q, lq, lscratch, queue[3], hand[3], pbox[3], pflag[3], perm, light, medium,
       giant, total;
+  long long hand0;
   size_t light_b, medium_b, giant_b;
   long long chunk, sub, pool[3];
   int light_blocks, medium_blocks, giant_blocks, lane_blocks;
@@ -545,7 +556,8 @@ Layout layout(long long n, long long mcmax, int giant_blocks, int sms, long long
   L.chunk = chunk;
   L.sub = sub;
   const long long pool = pool_boxes > 0 ? pool_boxes : kPoolDefault;
-  L.pool[0] = 0;
+  L.pool[0] = std::min(pool, chunk * kLaneArr);
+  L.hand0 = std::min(chunk, kLaneHandMax);
   L.pool[1] = std::min(pool, sub * 2 * LightCfg::QCAP);
   L.pool[2] = std::min(pool, sub * 2 * MediumCfg::QCAP);
   L.lane_blocks = (int)std::min<long long>((long long)TCCD_NMINB * sms, (chunk + kLaneNT - 1) / kLaneNT);
@@ -561,9 +573,11 @@ Layout layout(long long n, long long mcmax, int giant_blocks, int sms, long long
   L.light_q = o; o += align256((size_t)chunk * sizeof(Pre));
   L.lq = o; o += align256((size_t)chunk * sizeof(LaneRec));
   L.lscratch = o; o += align256((size_t)L.lane_blocks * kLaneNT * kLaneScratchWords * 8);
+  L.hand[0] = o; o += align256((size_t)L.hand0 * sizeof(Hand));
+  L.pbox[0] = o; o += align256((size_t)L.pool[0] * sizeof(Box));
+  L.pflag[0] = o; o += align256((size_t)L.pool[0]);
   // per sub-chunk
   L.queue[0] = L.light_q;
-  L.hand[0] = L.pbox[0] = L.pflag[0] = 0;
   for (int k = 1; k < 3; ++k) {
     L.queue[k] = o; o += align256((size_t)sub * sizeof(Pre));
     L.hand[k] = o; o += align256((size_t)sub * sizeof(Hand));
@@ -757,17 +771,16 @@ int tccd_solve_batch(const tccd_batch* b_in, void* stream) {
     io.in_base = from_light ? sub * L.sub : 0;
     io.in_limit = from_light ? L.sub : (long long)(1ull << 62);
     io.in_next = &ctr->q_next[tier];
-    io.in_hand = tier > 0 && !a.heavy_only ? (const Hand*)(ws + L.hand[tier]) : nullptr;
-    io.in_pbox = tier > 0 ? (const Box*)(ws + L.pbox[tier]) : nullptr;
-    io.in_pflag = tier > 0 ? (const uint8_t*)(ws + L.pflag[tier]) : nullptr;
+    // (light: the lane tier's handovers, indexed by the queue records)
+    io.in_hand = !a.heavy_only && (tier > 0 || lanes) ? (const Hand*)(ws + L.hand[tier]) : nullptr;
+    io.hand_in_record = tier == 0;
+    io.in_pbox = !a.heavy_only && (tier > 0 || lanes) ? (const Box*)(ws + L.pbox[tier]) : nullptr;
+    io.in_pflag = !a.heavy_only && (tier > 0 || lanes) ? (const uint8_t*)(ws + L.pflag[tier]) : nullptr;
     io.in_pool_cap = L.pool[tier];
     // (light tier: the lane tier's evictions restart there and are known to
     // reach levels above kLaneCap boxes: admit them as if they had that many)
-#ifndef TCCD_LIGHT_MAXSZ
-#define TCCD_LIGHT_MAXSZ 1
-#endif
     io.in_maxsz = a.heavy_only ? 1
-                  : (tier == 0 ? (lanes ? TCCD_LIGHT_MAXSZ : 1)
+                  : (tier == 0 ? (lanes ? kLaneArr : 1)
                                : 2 * (tier == 1 ? LightCfg::QCAP : MediumCfg::QCAP));
     io.in_perm = tier == 2 && !a.heavy_only ? (const unsigned int*)(ws + L.perm) : nullptr;
     io.perm_max = kOrderMax;
@@ -800,6 +813,13 @@ int tccd_solve_batch(const tccd_batch* b_in, void* stream) {
   lio.out = queue[0];
   lio.out_count = &ctr->light_count;
   lio.stats = ctr->lane;
+  lio.hand = (Hand*)(ws + L.hand[0]);
+  lio.hand_cap = L.hand0;
+  lio.hand_count = &ctr->lane_hand;
+  lio.pbox = (Box*)(ws + L.pbox[0]);
+  lio.pflag = (uint8_t*)(ws + L.pflag[0]);
+  lio.pool_cap = L.pool[0];
+  lio.pool_count = &ctr->lane_pool;
 
   // optional caller events, one after each stage launch, in launch order
   int n_ev = 0;

@@ -423,6 +423,7 @@ struct TierIO {
   unsigned long long* in_next;
   long long in_base;        // this launch's slice of the input queue
   long long in_limit;
+  int hand_in_record;       // in_hand indexed by Pre::pad (else by entry)
   long long in_pool_cap;    // boxes in the input handover pool
   Pre* out;                 // eviction queue of the next tier (nullptr: none)
   unsigned long long* out_count;
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
   // the next tier resumes the query; otherwise it restarts from the root.
   auto evict = [&](int s, int t) {
     const unsigned long long h = atomicAdd(io.out_count, 1ull);
-    io.out[h] = Pre{S.qidx[s], 0.0, 0u, 0u};
+    io.out[h] = Pre{S.qidx[s], 0.0, 0u, 0xffffffffu};
     long long off = -1;
     if (io.out_hand) {
       const unsigned long long o = atomicAdd(io.out_pool_count, (unsigned long long)t);
@@ -648,8 +649,19 @@ __global__ void __launch_bounds__(Cfg::NT, Cfg::MINB) engine_kernel(Args a, Tier
       long long off = -1;
       // (root widths; a handed-over level's below)
       S.w[s][0] = S.qp[s].t_max; S.w[s][1] = 1.0; S.w[s][2] = 1.0;
-      if (io.in_hand && io.in_hand[entry(S.admit_base + r)].n > 0) {
-        const Hand& hd = io.in_hand[entry(S.admit_base + r)];
+      // handover state: the entry's own slot (medium / giant queues), or the
+      // index the lane tier stored in the record (light queue)
+      long long hi = -1;
+      if (io.in_hand) {
+        if (io.hand_in_record) {
+          const unsigned int x = inq[entry(S.admit_base + r)].pad;
+          if (x != 0xffffffffu) hi = x;
+        } else {
+          hi = entry(S.admit_base + r);
+        }
+      }
+      if (hi >= 0 && io.in_hand[hi].n > 0) {
+        const Hand& hd = io.in_hand[hi];
         nr = hd.n;
         off = hd.off;
         {

@@ -33,9 +33,14 @@
 // into its shared-memory column with cp.async, one iteration apart, and
 // starts on it the iteration after, so neither stalls the warp.
 //
-// A query leaves this tier (and restarts from its root in the light tier:
-// exact, classification is a pure function of the box) when a level would
-// exceed kLaneCap boxes or the lattice would exceed its index range.
+// A query leaves this tier when its next level has more than kLaneCap
+// boxes (the level arrays hold 2 kLaneCap, so a level of at most kLaneCap
+// boxes always has room for its children): that level goes to the light
+// tier's handover pool, in visiting order with its run heads, with the
+// check count and first / drop records, and the light tier resumes the
+// query there.  If the handover pool is full, or the lattice would exceed
+// its index range, the query restarts from its root in the light tier
+// instead (exact: classification is a pure function of the box).
 #pragma once
 
 namespace tccd {
@@ -49,13 +54,15 @@ namespace tccd {
 #ifndef TCCD_NMINB
 #define TCCD_NMINB 3
 #endif
-constexpr int kLaneCap = TCCD_KL;  // boxes per level of a lane query
+constexpr int kLaneCap = TCCD_KL;  // largest level a lane processes
+constexpr int kLaneArr = 2 * kLaneCap;  // level array capacity: its children always fit
 constexpr int kLaneNT = TCCD_NNT;  // threads per CTA
 constexpr int kLaneMaxSplits = 52;  // per dimension: midpoints stay exact (indices < 2^53)
 constexpr int kLaneMaxLevel = 62;   // ti | ui | vi fits one 64-bit word
 // per-lane global scratch: two level arrays of words and two segment tables
-constexpr int kLaneSeg = kLaneCap / 2;
-constexpr int kLaneScratchWords = 2 * kLaneCap + kLaneSeg;  // (segment tables: 2 x u32 per word)
+// (a level's segments: at most one per refining box of the level before)
+constexpr int kLaneSeg = kLaneCap;
+constexpr int kLaneScratchWords = 2 * kLaneArr + kLaneSeg;  // (segment tables: 2 x u32 per word)
 
 // A query queued for the lane tier by the prologue: its root box is
 // non-disjoint and refined (one check done); its filters and kappas.
@@ -78,9 +85,17 @@ struct LaneIO {
   const unsigned long long* count;  // [2] entries per kind
   unsigned long long* next;         // [2] next entry to take per kind
   unsigned long long* scratch;      // [grid threads][kLaneScratchWords]
-  Pre* out;                         // light-tier queue (evicted queries restart there)
+  Pre* out;                         // light-tier queue (evicted queries go there)
   unsigned long long* out_count;
   unsigned long long* stats;        // [8] see Counters::lane
+  // handover to the light tier: state records and the pool of level boxes
+  Hand* hand;
+  long long hand_cap;
+  unsigned long long* hand_count;
+  Box* pbox;
+  uint8_t* pflag;
+  long long pool_cap;
+  unsigned long long* pool_count;
 };
 
 // this thread's column of a [kLaneCol][NT] shared array, read like an array
@@ -147,18 +162,33 @@ __device__ __forceinline__ void lane_write(const Args& a, long long q, bool use_
 }
 
 struct LaneStats {
-  unsigned long long cls = 0, checks = 0, done = 0, evicted = 0, wasted = 0;
+  unsigned int cls = 0, checks = 0, done = 0, evicted = 0, wasted = 0, handed = 0;
 };
+
+// add this warp's counters of one pass to the tier's (warp-reduced)
+template <int KIND>
+__device__ __forceinline__ void lane_flush(const LaneIO& io, const LaneStats& st) {
+  const unsigned int v[6] = {st.cls, st.checks, st.done, st.evicted, st.wasted, st.handed};
+  const int slot[6] = {KIND, 2 + KIND, 4 + KIND, 6, 7, 8};
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    unsigned long long x = v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&io.stats[slot[i]], x);
+  }
+}
 
 template <int KIND>
 __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, double* col,
-                                          unsigned long long* lb, LaneStats& st) {
+                                          unsigned long long* lb) {
+  LaneStats st;
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const ColP<kLaneNT> P{col};
   const ColP<kLaneNT> eps{col + kColEps * kLaneNT};
   const ColP<kLaneNT> kap{col + kColKap * kLaneNT};
-  unsigned int* const segs = reinterpret_cast<unsigned int*>(lb + 2 * kLaneCap);  // [2][kLaneSeg]
+  unsigned int* const segs = reinterpret_cast<unsigned int*>(lb + 2 * kLaneArr);  // [2][kLaneSeg]
   const unsigned long long total = io.count[KIND];
   bool dry = false;  // (warp-uniform) this kind's queue is empty
   int state = 0;     // 0 idle, 1 record in flight, 2 coordinates in flight, 3 active
@@ -169,7 +199,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   // level: split counts and widths of its boxes, its split dimension
   int L = 0, nt = 0, nu = 0, nv = 0, sd = 0;
   double wt = 1, wu = 1, wv = 1;
-  int cb = 0;        // current level array: lb + cb (the next one: lb + (cb ^ kLaneCap))
+  int cb = 0;        // current level array: lb + cb (the next one: lb + (cb ^ kLaneArr))
   int sgb = 0;       // current segment table: segs + sgb (the next one: segs + (sgb ^ kLaneSeg))
   int ncur = 0, k = 0;
   // visiting order of the current level: identity, or (after a t split)
@@ -184,27 +214,40 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   LaneRecBox fr{}, dr{};
   bool hf = false, hd = false;
 
+  // a warp-aggregated claim of queue entries for idle lanes: the atomic is
+  // issued in one iteration and its result read in the next, so its latency
+  // is spent classifying
+  unsigned claim_mask = 0;      // (warp-uniform) lanes a pending claim is for
+  int claim_leader = 0;
+  unsigned long long claim_base = 0;  // (the leader's register)
   for (;;) {
-    // ---- idle lanes claim a query (warp-aggregated) and start its copy
-    const unsigned need = __ballot_sync(FULL, state == 0);
-    if (need && !dry) {
-      const int leader = __ffs(need) - 1;
-      unsigned long long base = 0;
-      if (lane == leader) base = atomicAdd(&io.next[KIND], (unsigned long long)__popc(need));
-      base = __shfl_sync(FULL, base, leader);
-      if (base + __popc(need) >= total) dry = true;
-      if (state == 0) {
-        const unsigned long long kq = base + __popc(need & ((1u << lane) - 1u));
+    if (claim_mask) {
+      const unsigned long long base = __shfl_sync(FULL, claim_base, claim_leader);
+      if (base + __popc(claim_mask) >= total) dry = true;
+      if ((claim_mask >> lane) & 1u) {
+        const unsigned long long kq = base + __popc(claim_mask & ((1u << lane) - 1u));
         if (kq < total) {
+          // start the copy of the entry's record
           const double* src = reinterpret_cast<const double*>(
               &io.rec[KIND ? io.rec_cap - 1 - (long long)kq : (long long)kq]);
 #pragma unroll
           for (int i = 0; i < 8; ++i) cp_async8(col + (kColQ + i) * kLaneNT, src + i);
           state = 1;
+        } else {
+          state = 0;
         }
       }
+      claim_mask = 0;
+    }
+    const unsigned need = __ballot_sync(FULL, state == 0);
+    if (need && !dry) {
+      claim_leader = __ffs(need) - 1;
+      if (lane == claim_leader) claim_base = atomicAdd(&io.next[KIND], (unsigned long long)__popc(need));
+      claim_mask = need;
+      if (state == 0) state = 4;  // (claimed, the entry index arrives next iteration)
     }
     if (!__any_sync(FULL, state != 0)) break;
+    if (state == 4) continue;
     if (state == 1) {
       // the record has landed (one iteration later): copy the coordinates
       // and the per-query parameters
@@ -261,7 +304,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     // each somewhere else in its own query -- run it together; only the
     // writes of a finished query branch.
     unsigned long long* const cur = lb + cb;
-    unsigned long long* const nxt = lb + (cb ^ kLaneCap);
+    unsigned long long* const nxt = lb + (cb ^ kLaneArr);
     unsigned int* const snx = segs + (sgb ^ kLaneSeg);
     // the next box of this level: its word is loaded now, used next iteration
     const bool more = k + 1 < ncur;
@@ -328,7 +371,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     // u / v split only inside u + v <= 1 (_kernel.py:276-310); t-split
     // children are never clipped.
     const bool refine = !disj && !budget && !accept;
-    const bool evict = refine && nn + 2 > kLaneCap;
+    const bool evict = refine && nn + 2 > kLaneArr;  // (never: levels <= kLaneCap)
     const bool push = refine && !evict;
     const int pos = sd == 0 ? suv : (sd == 1 ? nv : 0);
     const unsigned long long lo = ((pk >> pos) << (pos + 1)) | (pk & ((1ull << pos) - 1ull));
@@ -375,7 +418,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       outcome = 1;
     }
     const bool nl = lvl_end && nn > 0;  // the next level becomes current
-    cb = nl ? cb ^ kLaneCap : cb;
+    cb = nl ? cb ^ kLaneArr : cb;
     sgb = nl ? sgb ^ kLaneSeg : sgb;
     const bool nilv = sd == 0;
     if (nl && nilv && nsn > 1) seg_mn = (int)segs[sgb + 1];
@@ -399,21 +442,64 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     nu += su_ ? 1 : 0; wu = su_ ? 0.5 * wu : wu;
     nv += sv_ ? 1 : 0; wv = sv_ ? 0.5 * wv : wv;
     const int ns = sd == 0 ? nt : (sd == 1 ? nu : nv);
-    outcome = nl && (ns > kLaneMaxSplits || L > kLaneMaxLevel) ? 2 : outcome;
+    // a level too large for this tier (or a lattice about to leave its index
+    // range) is handed over to the light tier
+    outcome = nl && (ncur > kLaneCap || ns > kLaneMaxSplits || L > kLaneMaxLevel) ? 3 : outcome;
     sd = nl ? lane_split_dim(wt, wu, wv, kapr) : sd;
     if (outcome == 1) {
-      st.checks += (unsigned long long)(C - 1);  // checks of finished queries (root: prologue's)
+      st.checks += (unsigned)(C - 1);  // checks of finished queries (root: prologue's)
       st.done += 1;
       state = 0;
-    } else if (outcome == 2) {
-      // restart from the root in the light tier (one self-contained record)
-      const unsigned long long h = atomicAdd(io.out_count, 1ull);
-      io.out[h] = Pre{q, 0.0, 0u, 0u};
+    } else if (outcome >= 2) {
+      // to the light tier: with the current level handed over (outcome 3,
+      // room permitting), else restarting from the root
+      unsigned int hidx = 0xffffffffu;
+      if (outcome == 3) {
+        const unsigned long long h = atomicAdd(io.hand_count, 1ull);
+        const unsigned long long off = atomicAdd(io.pool_count, (unsigned long long)ncur);
+        if ((long long)h < io.hand_cap && (long long)(off + ncur) <= io.pool_cap) {
+          hidx = (unsigned int)h;
+          const unsigned long long* cw = lb + cb;
+          int ss = 0, sm = seg_m, sk = 0, si = 0;
+          double prev = -1.0;
+          for (int j = 0; j < ncur; ++j) {
+            int pos = j;
+            if (ilv) {
+              if (sk == 2 * sm) { ss += 2 * sm; ++si; sm = (int)segs[sgb + si]; sk = 0; }
+              pos = sk < sm ? ss + 2 * sk : ss + 2 * (sk - sm) + 1;
+              ++sk;
+            }
+            const Box bb = lane_box(cw[pos], nt, nu, nv, t_max);
+            io.pbox[off + j] = bb;
+            io.pflag[off + j] = (uint8_t)(j == 0 || bb.t0 != prev ? 128 : 0);  // the engine's kHead
+            prev = bb.t0;
+          }
+          Hand& H = io.hand[h];
+          H.C = C;
+          H.off = (long long)off;
+          H.level = L;
+          H.n = ncur;
+          H.rec[0].b = lane_box(fr.pk, fr.shape & 255, (fr.shape >> 8) & 255, fr.shape >> 16, t_max);
+          H.rec[0].codom = fr.codom;
+          H.rec[0].level = fr.level;
+          H.rec[1].b = lane_box(dr.pk, dr.shape & 255, (dr.shape >> 8) & 255, dr.shape >> 16, t_max);
+          H.rec[1].codom = dr.codom;
+          H.rec[1].level = dr.level;
+          H.have_first = hf ? 1 : 0;
+          H.have_drop = hd ? 1 : 0;
+          st.handed += 1;
+        }
+      }
+      const unsigned long long e = atomicAdd(io.out_count, 1ull);
+      io.out[e] = Pre{q, 0.0, 0u, hidx};
       st.evicted += 1;
-      st.wasted += (unsigned long long)(C - 1);  // lane checks that the light tier repeats
+      // (a restart repeats the lane's checks in the light tier)
+      if (hidx == 0xffffffffu) st.wasted += (unsigned)(C - 1);
+      else st.checks += (unsigned)(C - 1);  // (on the reference's path: the light tier goes on)
       state = 0;
     }
   }
+  lane_flush<KIND>(io, st);
 }
 
 __global__ void __launch_bounds__(kLaneNT, TCCD_NMINB) lane_kernel(Args a, LaneIO io) {
@@ -426,19 +512,9 @@ __global__ void __launch_bounds__(kLaneNT, TCCD_NMINB) lane_kernel(Args a, LaneI
   // their queues; a warp whose queue runs dry moves to the other one
   const long long gw = gt >> 5, nw = (long long)gridDim.x * (kLaneNT / 32);
   int kind = (nvf + nee) > 0 && (unsigned long long)gw * (nvf + nee) < nee * (unsigned long long)nw;
-  LaneStats s0, s1;
   for (int pass = 0; pass < 2; ++pass, kind ^= 1) {
-    if (kind == 0) lane_loop<0>(a, io, col, lb, s0);
-    else lane_loop<1>(a, io, col, lb, s1);
-  }
-  const unsigned long long v[8] = {s0.cls, s1.cls, s0.checks, s1.checks, s0.done, s1.done,
-                                   s0.evicted + s1.evicted, s0.wasted + s1.wasted};
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    unsigned long long x = v[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&io.stats[i], x);
+    if (kind == 0) lane_loop<0>(a, io, col, lb);
+    else lane_loop<1>(a, io, col, lb);
   }
 }
 

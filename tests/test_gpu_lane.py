@@ -71,6 +71,8 @@ def test_lane_tier_takes_the_shallow_queries(cuda):
     assert entered == done + ev
     assert entered > 0.3 * w.n
     assert ev < 0.05 * entered
+    # with room in the handover pool every eviction carries its level
+    assert st[_lib.STAT_LANE_HANDED] == ev and st[_lib.STAT_LANE_WASTED] == 0
 
 
 @pytest.mark.parametrize("config,count,kw", [(3, 100_000, {}), (1, 20_000, {}),
@@ -90,8 +92,10 @@ def test_algorithmic_check_accounting(cuda, config, count, kw):
     assert st[_lib.STAT_RESTARTS] == 0 and st[_lib.STAT_RESTARTS + 1] == 0
     valid = r["status"].numpy() < 2
     root_decided = st[_lib.STAT_PROLOGUE_DONE] - int((~valid).sum())
+    # (each lane query's root check is the prologue's: one per query the lane
+    # tier finished or handed over)
     total = (root_decided + st[_lib.STAT_LANE_CHECKS] + st[_lib.STAT_LANE_CHECKS + 1]
-             + st[_lib.STAT_LANE_DONE] + st[_lib.STAT_LANE_DONE + 1]
+             + st[_lib.STAT_LANE_DONE] + st[_lib.STAT_LANE_DONE + 1] + st[_lib.STAT_LANE_HANDED]
              + st[_lib.STAT_TIER_CHECKS:_lib.STAT_TIER_CHECKS + 3].sum())
     assert total == int(checks[valid].sum())
 
