@@ -263,9 +263,13 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long
     if (st != kHit) {
       write_result(a, q, st, root, 0.0, 0, 0, 0);
     } else {
-      kappas(P, qp.kind, qp.t_max, qp.kap);
+      // one evaluation of F at the domain's corners gives the kappas and the
+      // root box's hull
+      double F[8][3];
+      root_corners(P, qp.kind, qp.t_max, F);
+      kappas_from(F, qp.kap);
       double wb;
-      const int cls = classify(P, qp.kind, root, qp.eps, qp.sep, wb, qp.tame != 0);
+      const int cls = classify_root(F, qp.eps, qp.sep, wb);
       if (cls == kDisjoint) {
         // the queue empties after one check (_kernel.py:188-199, 321-324)
         write_result(a, q, kFree, root, 0.0, 1, 0, 0);

@@ -206,6 +206,86 @@ __device__ __forceinline__ int tame_coords(PtrT P) {
   return ok ? 1 : 0;
 }
 
+// F at the 8 corners of the domain [0, t_max] x [0,1]^2, corner index
+// 4 t + 2 u + v: the values _kernel._kappas differences (_kernel.py:98-132)
+// and, bit for bit, the 8 corner values _hull_axis takes of the root box
+// (the same operations: a lerp with t in {0, t_max}, then (1 - u) - v with
+// u, v in {0, 1}).
+template <typename PtrT>
+__device__ __forceinline__ void root_corners(PtrT P, int kind, double t_max, double F[8][3]) {
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const double t = it ? t_max : 0.0;
+    const double omt = 1.0 - t;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const double a = omt * P[ax] + t * P[12 + ax];
+      const double b = omt * P[3 + ax] + t * P[15 + ax];
+      const double c = omt * P[6 + ax] + t * P[18 + ax];
+      const double d = omt * P[9 + ax] + t * P[21 + ax];
+#pragma unroll
+      for (int iu = 0; iu < 2; ++iu)
+#pragma unroll
+        for (int iv = 0; iv < 2; ++iv) {
+          const double u = iu ? 1.0 : 0.0, v = iv ? 1.0 : 0.0;
+          double val;
+          if (kind == 0) val = a - ((1.0 - u - v) * b + u * c + v * d);
+          else val = ((1.0 - u) * a + u * b) - ((1.0 - v) * c + v * d);
+          F[4 * it + 2 * iu + iv][ax] = val;
+        }
+    }
+  }
+}
+
+// kappas from the domain's corner values (strides t=4, u=2, v=1)
+__device__ __forceinline__ void kappas_from(const double F[8][3], double out[3]) {
+  const int strides[3] = {4, 2, 1};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double best = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i & strides[k]) continue;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        const double d = fabs(F[i + strides[k]][ax] - F[i][ax]);
+        if (d > best) best = d;
+      }
+    }
+    out[k] = 3.0 * best;
+  }
+}
+
+// _kernel._classify of the root box from its corner values: the same
+// comparisons as classify_k (the hull ignores NaN like the reference's
+// `val < mn` / `val > mx` updates)
+__device__ __forceinline__ int classify_root(const double F[8][3], const double* eps, double sep,
+                                             double& wb) {
+  bool contained = true;
+  double width = 0.0;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    double mn = __longlong_as_double(0x7ff0000000000000LL);
+    double mx = __longlong_as_double((long long)0xfff0000000000000ULL);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      mn = fmin(mn, F[k][ax]);
+      mx = fmax(mx, F[k][ax]);
+    }
+    const double e = eps[ax];
+    const double lo = mn - sep, hi = mx + sep;
+    if (lo > e || hi < -e) {
+      wb = 0.0;
+      return kDisjoint;
+    }
+    if (!(lo >= -e && hi <= e)) contained = false;
+    const double d = mx - mn;
+    if (d > width) width = d;
+  }
+  wb = width;
+  return contained ? kContained : kIntersects;
+}
+
 // _kernel._kappas (_kernel.py:98-132): 3 * max |F(corner + stride) - F(corner)|
 // over the domain [0, t_max] x [0,1]^2, strides t=4, u=2, v=1.
 template <typename PtrT>
