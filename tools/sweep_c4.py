@@ -11,7 +11,7 @@ seconds) and says which.  The CPU port (oracle/, all host threads) is timed on
 a small prefix of the same sample and checked bit-exact against the GPU
 results on it.
 
-    python tools/sweep_c4.py [--full] [--out profiles/r01/sweep_c4.jsonl]
+    python tools/sweep_c4.py [--full] [--out profiles/r02/sweep_c4.jsonl]
 """
 import argparse
 import json
@@ -26,7 +26,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import oracle  # noqa: E402  (test infrastructure: CPU baseline + parity check only)
-from paper_2009_13349_b200 import solve_batch  # noqa: E402
+from paper_2009_13349_b200 import _lib, solve_batch  # noqa: E402
 from paper_2009_13349_b200 import workloads as W  # noqa: E402
 
 F_CHECK = {0: 200, 1: 174}
@@ -45,7 +45,7 @@ args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
 threads = len(os.sched_getaffinity(0))
-base = W.generate(4, 0, W.CONFIGS[4]["n"] if args.full else int(max(DEFAULT_N.values()) * args.scale))
+base = W.generate_parallel(4, 0, W.CONFIGS[4]["n"] if args.full else int(max(DEFAULT_N.values()) * args.scale))
 pts_all = torch.from_numpy(base.points).to(dev)
 kind_all = torch.from_numpy(base.kind).to(dev)
 rows = []
@@ -90,7 +90,11 @@ for d in SEPS:
            "mean_checks": float(checks.mean()), "max_checks": int(checks.max()),
            "checks_per_s": float(checks.sum()) / t,
            "solve_tflops": flops / t / 1e12,
-           "boxes_per_tier": s[4:7], "medium_tier_queries": s[3], "giant_tier_queries": s[0],
+           "boxes_per_tier": s[_lib.STAT_BOXES:_lib.STAT_BOXES + 3],
+           "lane_queries": s[_lib.STAT_LANE_QUERIES], "lane_handed_over": s[_lib.STAT_LANE_HANDED],
+           "medium_tier_queries": s[_lib.STAT_MEDIUM_QUERIES],
+           "giant_tier_queries": s[_lib.STAT_GIANT_QUERIES],
+           "handover_restarts": s[_lib.STAT_RESTARTS:_lib.STAT_RESTARTS + 2],
            "cpu_port": {"queries": nc, "threads": threads, "queries_per_s": nc / tc,
                         "bit_exact_vs_gpu": bool(same)}}
     rows.append(row)
