@@ -1,26 +1,29 @@
 // libtccd: batched Tight-Inclusion CCD on B200 (sm_100a), FP64, FMA-free.
 //
 // Reproduces the reference state machine (ccdkit._kernel.solve_kernel,
-// pkg/src/ccdkit/_kernel.py:136-324) exactly for every query of a batch:
+// pkg/src/ccdkit/_kernel.py:136-324) exactly for every query of a batch.
+// Per library chunk (<= kChunk queries):
 //
 //  1. prologue_kernel, one thread per query: coalesced load of the 24
 //     coordinates, parameter validation (core.py:176-184), filters
-//     (inclusion.py:85-122), kappas (_kernel.py:98-132) and the root-box
-//     check.  Queries decided at the root (about half of random inputs) are
-//     written out; the rest are compacted into the light tier's queue with
-//     their filters, kappas and root class precomputed.
-//  2. engine_kernel tiers (tccd_engine.cuh), each a persistent grid whose
-//     independent groups keep several queries resident and advance them one
-//     BFS level per round with lane-per-box classification:
-//        light  : 128-thread CTA (5 per SM), 40 queries, levels <= 1024
+//     (inclusion.py:85-122), one evaluation of F at the domain's corners for
+//     the kappas (_kernel.py:98-132) and the root-box check.  Queries decided
+//     at the root are written out; survivors go to the lane queue (dyadic
+//     t_max, tame coordinates) or the light queue.
+//  2. lane_kernel (tccd_lane.cuh): one query per thread, box by box in the
+//     reference's visiting order, for queries whose levels stay within 64
+//     boxes; larger levels are handed over to the light tier.
+//  3. engine_kernel tiers (tccd_engine.cuh) over the light queue, in
+//     sub-chunks of <= kSub entries: persistent grids whose independent
+//     groups keep several queries resident and advance them one BFS level
+//     per round with lane-per-box classification:
+//        light  : 128-thread CTA (5 per SM), 16 queries, levels <= 1024
 //                 boxes, per-box bookkeeping in shared memory
 //        medium : 256-thread CTA (2 per SM), 8 queries, levels <= 8192
 //                 boxes, per-box bookkeeping in shared memory
 //        giant  : 512-thread CTA per query, levels up to 2 * m_I boxes
-//     A query whose level outgrows its tier moves to the next tier with its
-//     next level handed over (or restarts there if the handover pool is full).
-//
-// The host splits large batches into chunks (bounded queue memory).
+//     A query whose level outgrows its tier moves to the next tier with that
+//     level handed over (or restarts there if the handover pool is full).
 #include <cuda_runtime.h>
 
 #include <climits>
