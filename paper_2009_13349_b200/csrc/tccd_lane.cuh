@@ -59,6 +59,10 @@ constexpr int kLaneArr = 2 * kLaneCap;  // level array capacity: its children al
 constexpr int kLaneNT = TCCD_NNT;  // threads per CTA
 constexpr int kLaneMaxSplits = 52;  // per dimension: midpoints stay exact (indices < 2^53)
 constexpr int kLaneMaxLevel = 62;   // ti | ui | vi fits one 64-bit word
+#ifndef TCCD_LANE_TAIL
+#define TCCD_LANE_TAIL 128
+#endif
+constexpr int kLaneTailChecks = TCCD_LANE_TAIL;  // (tail handover threshold)
 // per-lane global scratch: two level arrays of words and two segment tables
 // (a level's segments: at most one per refining box of the level before)
 constexpr int kLaneSeg = kLaneCap;
@@ -443,8 +447,13 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     nv += sv_ ? 1 : 0; wv = sv_ ? 0.5 * wv : wv;
     const int ns = sd == 0 ? nt : (sd == 1 ? nu : nv);
     // a level too large for this tier (or a lattice about to leave its index
-    // range) is handed over to the light tier
-    outcome = nl && (ncur > kLaneCap || ns > kLaneMaxSplits || L > kLaneMaxLevel) ? 3 : outcome;
+    // range) is handed over to the light tier; so is, once this kind's queue
+    // is empty, the level of a query that has already run a while: the
+    // lane tier's tail (lanes idle while the last queries finish one box at
+    // a time) becomes level-parallel work for the light tier
+    outcome = nl && (ncur > kLaneCap || ns > kLaneMaxSplits || L > kLaneMaxLevel ||
+                     (dry && C >= kLaneTailChecks))
+                  ? 3 : outcome;
     sd = nl ? lane_split_dim(wt, wu, wv, kapr) : sd;
     if (outcome == 1) {
       st.checks += (unsigned)(C - 1);  // checks of finished queries (root: prologue's)
