@@ -52,7 +52,7 @@ namespace tccd {
 #define TCCD_NNT 128
 #endif
 #ifndef TCCD_NMINB
-#define TCCD_NMINB 3
+#define TCCD_NMINB 4
 #endif
 constexpr int kLaneCap = TCCD_KL;  // largest level a lane processes
 constexpr int kLaneArr = 2 * kLaneCap;  // level array capacity: its children always fit
@@ -78,10 +78,12 @@ struct LaneRec {
 };
 static_assert(sizeof(LaneRec) == 64, "LaneRec layout");
 // shared-memory column of one lane: the 24 coordinates, the LaneRec words,
-// the per-query parameters
-constexpr int kLaneCol = 36;
+// the per-query parameters, and the first / drop records (lattice word,
+// codomain width, split counts | level << 24) -- read only when a query
+// ends, so they do not hold registers
+constexpr int kLaneCol = 42;
 constexpr int kColQ = 24, kColWb = 25, kColEps = 26, kColKap = 29, kColSep = 32, kColDelta = 33,
-              kColTmax = 34, kColMc = 35;
+              kColTmax = 34, kColMc = 35, kColFr = 36, kColDr = 39;
 
 struct LaneIO {
   const LaneRec* rec;             // vertex-face entries from the front, edge-edge from the back
@@ -146,33 +148,44 @@ __device__ __forceinline__ int lane_split_dim(double wt, double wu, double wv, K
   return sd;
 }
 
-// a recorded box (first / drop): lattice word, split counts, level, width, t_lo
-struct LaneRecBox {
-  unsigned long long pk;
-  int shape;  // nt | nu << 8 | nv << 16
-  int level;
-  double codom;
-  double t0;
-};
+// a recorded box in a lane's column (kColFr / kColDr): lattice word, width,
+// split counts nt | nu << 8 | nv << 16 | level << 24
+__device__ __forceinline__ void lane_record(double* col, int at, unsigned long long pk, double codom,
+                                            int meta) {
+  col[at * kLaneNT] = __longlong_as_double((long long)pk);
+  col[(at + 1) * kLaneNT] = codom;
+  col[(at + 2) * kLaneNT] = __longlong_as_double((long long)meta);
+}
 
-// write record x (or y when !use_x), field by field (no addressable copy)
-__device__ __forceinline__ void lane_write(const Args& a, long long q, bool use_x,
-                                           const LaneRecBox& x, const LaneRecBox& y,
-                                           double t_max, long long checks, int early) {
-  const unsigned long long pk = use_x ? x.pk : y.pk;
-  const int shape = use_x ? x.shape : y.shape;
-  const Box b = lane_box(pk, shape & 255, (shape >> 8) & 255, shape >> 16, t_max);
-  write_result(a, q, kHit, b, use_x ? x.codom : y.codom, checks, early, use_x ? x.level : y.level);
+__device__ __forceinline__ Box lane_record_box(const double* col, int at, double t_max) {
+  const unsigned long long pk = (unsigned long long)__double_as_longlong(col[at * kLaneNT]);
+  const int m = (int)__double_as_longlong(col[(at + 2) * kLaneNT]);
+  return lane_box(pk, m & 255, (m >> 8) & 255, (m >> 16) & 255, t_max);
+}
+
+__device__ __forceinline__ int lane_record_level(const double* col, int at) {
+  return (int)__double_as_longlong(col[(at + 2) * kLaneNT]) >> 24;
+}
+
+// the result of a query that ends on the record at column offset `at`
+__device__ __forceinline__ void lane_write(const Args& a, const double* col, int at,
+                                           long long checks, int early) {
+  const long long q = __double_as_longlong(col[kColQ * kLaneNT]);
+  const double t_max = col[kColTmax * kLaneNT];
+  write_result(a, q, kHit, lane_record_box(col, at, t_max), col[(at + 1) * kLaneNT], checks,
+               early, lane_record_level(col, at));
 }
 
 struct LaneStats {
-  unsigned int cls = 0, checks = 0, done = 0, evicted = 0, wasted = 0, handed = 0;
+  unsigned int checks = 0, done = 0, evicted = 0, wasted = 0, handed = 0;
 };
 
 // add this warp's counters of one pass to the tier's (warp-reduced)
 template <int KIND>
 __device__ __forceinline__ void lane_flush(const LaneIO& io, const LaneStats& st) {
-  const unsigned int v[6] = {st.cls, st.checks, st.done, st.evicted, st.wasted, st.handed};
+  // (classifications: the checks on the reference's path + the ones repeated)
+  const unsigned int v[6] = {st.checks + st.wasted, st.checks, st.done, st.evicted, st.wasted,
+                             st.handed};
   const int slot[6] = {KIND, 2 + KIND, 4 + KIND, 6, 7, 8};
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
@@ -197,9 +210,8 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   bool dry = false;  // (warp-uniform) this kind's queue is empty
   int state = 0;     // 0 idle, 1 record in flight, 2 coordinates in flight, 3 active
   // query
-  long long q = 0, mc = 0, C = 0;
-  double sep = 0, delta = 0, t_max = 1;
-  double kapr[3] = {0, 0, 0};  // kappas (registers: every level end reads them)
+  int mc = 0, C = 0;  // (a lane query stays far below 2^31 checks: <= 62 levels of <= 64 boxes)
+  double sep = 0, delta = 0;
   // level: split counts and widths of its boxes, its split dimension
   int L = 0, nt = 0, nu = 0, nv = 0, sd = 0;
   double wt = 1, wu = 1, wv = 1;
@@ -215,7 +227,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   int nn = 0, nsn = 0, run_m = 0, seg0 = 0;
   unsigned long long run = ~0ull, nxt0 = 0;
   bool col_lvl = false;  // this level has had a non-disjoint box (last_colliding_level)
-  LaneRecBox fr{}, dr{};
+  double fr_t0 = 0, dr_t0 = 0;  // t_lo of the first / drop records (the rest: in the column)
   bool hf = false, hd = false;
 
   // a warp-aggregated claim of queue entries for idle lanes: the atomic is
@@ -273,21 +285,23 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     }
     if (state == 2) {
       cp_async_wait_all();
-      q = __double_as_longlong(col[kColQ * kLaneNT]);
-      mc = __double_as_longlong(col[kColMc * kLaneNT]);
+      {
+        const long long m = __double_as_longlong(col[kColMc * kLaneNT]);
+        mc = m < 0x7fffffffLL ? (int)m : 0x7fffffff;
+      }
       sep = col[kColSep * kLaneNT];
       delta = col[kColDelta * kLaneNT];
-      t_max = col[kColTmax * kLaneNT];
-      kapr[0] = kap[0]; kapr[1] = kap[1]; kapr[2] = kap[2];
+      const double t_max = col[kColTmax * kLaneNT];
       // the root (level 0, one check, the prologue's) is the first record
       // and was refined: level 1 = its two children (never clipped: a root
       // child's lower corner is 0)
-      fr.pk = 0; fr.shape = 0; fr.level = 0; fr.codom = col[kColWb * kLaneNT]; fr.t0 = 0.0;
+      lane_record(col, kColFr, 0ull, col[kColWb * kLaneNT], 0);
+      fr_t0 = 0.0;
       hf = true; hd = false;
       C = 1;
       nt = nu = nv = 0;
       wt = t_max; wu = 1.0; wv = 1.0;
-      const int s0 = lane_split_dim(wt, wu, wv, kapr);
+      const int s0 = lane_split_dim(wt, wu, wv, kap);
       if (s0 == 0) { nt = 1; wt *= 0.5; } else if (s0 == 1) { nu = 1; wu *= 0.5; } else { nv = 1; wv *= 0.5; }
       cb = 0; sgb = 0;
       lb[0] = 0ull;
@@ -298,7 +312,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       pk = 0; pk_next = 1;
       nn = 0; nsn = 0; run_m = 0; seg0 = 0; run = ~0ull; nxt0 = 0;
       col_lvl = false;
-      sd = lane_split_dim(wt, wu, wv, kapr);
+      sd = lane_split_dim(wt, wu, wv, kap);
       state = 3;
     }
     if (state != 3) continue;  // (idle: this kind's queue ran dry)
@@ -337,18 +351,14 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     double wb;
     const int cls = classify_full<KIND>(P, b, eps, sep, wb);
     ++C;
-    ++st.cls;
     const bool disj = cls == kDisjoint;
     const bool budget = C >= mc;
     const bool accept = !disj && (wb < delta || cls == kContained);  // (:215)
     // first colliding box of this level (:201-206)
-    const int shape = nt | (nu << 8) | (nv << 16);
+    const int meta = nt | (nu << 8) | (nv << 16) | (L << 24);
     const bool first = !disj && !col_lvl;
-    fr.pk = first ? pk : fr.pk;
-    fr.shape = first ? shape : fr.shape;
-    fr.level = first ? L : fr.level;
-    fr.codom = first ? wb : fr.codom;
-    fr.t0 = first ? b.t0 : fr.t0;
+    if (first) lane_record(col, kColFr, pk, wb, meta);
+    fr_t0 = first ? b.t0 : fr_t0;
     hf = hf || first;
     // the ways this box can end the query
     const bool end_disj = disj && budget && (hd || more || nn > 0);   // (:188-199)
@@ -356,19 +366,16 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     const bool end_acc = accept && !budget && !col_lvl;               // (:243-252)
     int outcome = 0;  // 0 continue, 1 ended (result written), 2 evict
     if (end_disj || end_budget || end_acc) {
-      const LaneRecBox me{pk, shape, L, wb, b.t0};
-      const bool use_drop = hd && (end_acc ? dr.t0 < b.t0
-                                           : (end_disj ? (!hf || dr.t0 < fr.t0) : dr.t0 < fr.t0));
-      lane_write(a, q, use_drop, dr, end_acc ? me : fr, t_max, C, end_acc ? 0 : 1);
+      const bool use_drop = hd && (end_acc ? dr_t0 < b.t0
+                                           : (end_disj ? (!hf || dr_t0 < fr_t0) : dr_t0 < fr_t0));
+      // (an accepted first box of its level: the record just written is it)
+      lane_write(a, col, use_drop ? kColDr : kColFr, C, end_acc ? 0 : 1);
       outcome = 1;
     }
     // an accepted box after the level's first: the drop record (:253-258)
-    const bool drop = accept && !budget && col_lvl && (!hd || b.t0 < dr.t0);
-    dr.pk = drop ? pk : dr.pk;
-    dr.shape = drop ? shape : dr.shape;
-    dr.level = drop ? L : dr.level;
-    dr.codom = drop ? wb : dr.codom;
-    dr.t0 = drop ? b.t0 : dr.t0;
+    const bool drop = accept && !budget && col_lvl && (!hd || b.t0 < dr_t0);
+    if (drop) lane_record(col, kColDr, pk, wb, meta);
+    dr_t0 = drop ? b.t0 : dr_t0;
     hd = hd || drop;
     // refine along the level's split dimension: insert the child bit; the
     // children are stored in push order.  Vertex-face: the upper child of a
@@ -414,10 +421,10 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     if (lvl_end && nn == 0) {
       // queue exhausted (_kernel.py:321-324)
       if (hd) {
-        lane_write(a, q, true, dr, dr, t_max, C, 0);
+        lane_write(a, col, kColDr, C, 0);
       } else {
         const Box z = {0, 0, 0, 0, 0, 0};
-        write_result(a, q, kFree, z, 0.0, C, 0, 0);
+        write_result(a, __double_as_longlong(col[kColQ * kLaneNT]), kFree, z, 0.0, C, 0, 0);
       }
       outcome = 1;
     }
@@ -454,7 +461,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     outcome = nl && (ncur > kLaneCap || ns > kLaneMaxSplits || L > kLaneMaxLevel ||
                      (dry && C >= kLaneTailChecks))
                   ? 3 : outcome;
-    sd = nl ? lane_split_dim(wt, wu, wv, kapr) : sd;
+    sd = nl ? lane_split_dim(wt, wu, wv, kap) : sd;
     if (outcome == 1) {
       st.checks += (unsigned)(C - 1);  // checks of finished queries (root: prologue's)
       st.done += 1;
@@ -478,7 +485,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
               pos = sk < sm ? ss + 2 * sk : ss + 2 * (sk - sm) + 1;
               ++sk;
             }
-            const Box bb = lane_box(cw[pos], nt, nu, nv, t_max);
+            const Box bb = lane_box(cw[pos], nt, nu, nv, col[kColTmax * kLaneNT]);
             io.pbox[off + j] = bb;
             io.pflag[off + j] = (uint8_t)(j == 0 || bb.t0 != prev ? 128 : 0);  // the engine's kHead
             prev = bb.t0;
@@ -488,19 +495,20 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
           H.off = (long long)off;
           H.level = L;
           H.n = ncur;
-          H.rec[0].b = lane_box(fr.pk, fr.shape & 255, (fr.shape >> 8) & 255, fr.shape >> 16, t_max);
-          H.rec[0].codom = fr.codom;
-          H.rec[0].level = fr.level;
-          H.rec[1].b = lane_box(dr.pk, dr.shape & 255, (dr.shape >> 8) & 255, dr.shape >> 16, t_max);
-          H.rec[1].codom = dr.codom;
-          H.rec[1].level = dr.level;
+          const double t_max = col[kColTmax * kLaneNT];
+          H.rec[0].b = lane_record_box(col, kColFr, t_max);
+          H.rec[0].codom = col[(kColFr + 1) * kLaneNT];
+          H.rec[0].level = lane_record_level(col, kColFr);
+          H.rec[1].b = lane_record_box(col, kColDr, t_max);
+          H.rec[1].codom = col[(kColDr + 1) * kLaneNT];
+          H.rec[1].level = lane_record_level(col, kColDr);
           H.have_first = hf ? 1 : 0;
           H.have_drop = hd ? 1 : 0;
           st.handed += 1;
         }
       }
       const unsigned long long e = atomicAdd(io.out_count, 1ull);
-      io.out[e] = Pre{q, 0.0, 0u, hidx};
+      io.out[e] = Pre{__double_as_longlong(col[kColQ * kLaneNT]), 0.0, 0u, hidx};
       st.evicted += 1;
       // (a restart repeats the lane's checks in the light tier)
       if (hidx == 0xffffffffu) st.wasted += (unsigned)(C - 1);
