@@ -63,6 +63,10 @@ constexpr int kLaneMaxLevel = 62;   // ti | ui | vi fits one 64-bit word
 #define TCCD_LANE_TAIL 128
 #endif
 constexpr int kLaneTailChecks = TCCD_LANE_TAIL;  // (tail handover threshold)
+#ifndef TCCD_LANE_CLAIM
+#define TCCD_LANE_CLAIM 32
+#endif
+constexpr int kLaneClaim = TCCD_LANE_CLAIM;  // queue entries a warp claims at once
 // per-lane global scratch: two level arrays of words and two segment tables
 // (a level's segments: at most one per refining box of the level before)
 constexpr int kLaneSeg = kLaneCap;
@@ -167,13 +171,18 @@ __device__ __forceinline__ int lane_record_level(const double* col, int at) {
   return (int)__double_as_longlong(col[(at + 2) * kLaneNT]) >> 24;
 }
 
+__device__ __forceinline__ void lane_emit(const Args& a, long long q, uint8_t status, Box b,
+                                       double codom, long long checks, int early, int level) {
+  write_result(a, q, status, b, codom, checks, early, level);
+}
+
 // the result of a query that ends on the record at column offset `at`
 __device__ __forceinline__ void lane_write(const Args& a, const double* col, int at,
                                            long long checks, int early) {
   const long long q = __double_as_longlong(col[kColQ * kLaneNT]);
   const double t_max = col[kColTmax * kLaneNT];
-  write_result(a, q, kHit, lane_record_box(col, at, t_max), col[(at + 1) * kLaneNT], checks,
-               early, lane_record_level(col, at));
+  lane_emit(a, q, kHit, lane_record_box(col, at, t_max), col[(at + 1) * kLaneNT], checks, early,
+            lane_record_level(col, at));
 }
 
 struct LaneStats {
@@ -181,12 +190,11 @@ struct LaneStats {
 };
 
 // add this warp's counters of one pass to the tier's (warp-reduced)
-template <int KIND>
-__device__ __forceinline__ void lane_flush(const LaneIO& io, const LaneStats& st) {
+__device__ __forceinline__ void lane_flush(const LaneIO& io, const LaneStats& st, int kind) {
   // (classifications: the checks on the reference's path + the ones repeated)
   const unsigned int v[6] = {st.checks + st.wasted, st.checks, st.done, st.evicted, st.wasted,
                              st.handed};
-  const int slot[6] = {KIND, 2 + KIND, 4 + KIND, 6, 7, 8};
+  const int slot[6] = {kind, 2 + kind, 4 + kind, 6, 7, 8};
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     unsigned long long x = v[i];
@@ -196,9 +204,10 @@ __device__ __forceinline__ void lane_flush(const LaneIO& io, const LaneStats& st
   }
 }
 
-template <int KIND>
+// One kind's queue (kind is warp-uniform; only the classification is
+// specialized on it, so the loop's code exists once).
 __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, double* col,
-                                          unsigned long long* lb) {
+                                          unsigned long long* lb, const int kind) {
   LaneStats st;
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -206,7 +215,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   const ColP<kLaneNT> eps{col + kColEps * kLaneNT};
   const ColP<kLaneNT> kap{col + kColKap * kLaneNT};
   unsigned int* const segs = reinterpret_cast<unsigned int*>(lb + 2 * kLaneArr);  // [2][kLaneSeg]
-  const unsigned long long total = io.count[KIND];
+  const unsigned long long total = io.count[kind];
   bool dry = false;  // (warp-uniform) this kind's queue is empty
   int state = 0;     // 0 idle, 1 record in flight, 2 coordinates in flight, 3 active
   // query
@@ -230,40 +239,58 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   double fr_t0 = 0, dr_t0 = 0;  // t_lo of the first / drop records (the rest: in the column)
   bool hf = false, hd = false;
 
-  // a warp-aggregated claim of queue entries for idle lanes: the atomic is
-  // issued in one iteration and its result read in the next, so its latency
-  // is spent classifying
-  unsigned claim_mask = 0;      // (warp-uniform) lanes a pending claim is for
-  int claim_leader = 0;
-  unsigned long long claim_base = 0;  // (the leader's register)
+  // The warp claims queue entries kLaneClaim at a time (one atomic on the
+  // kind's counter per range, not per query) and hands them to its idle
+  // lanes; the next range is claimed while the current one still lasts, and
+  // the atomic's result is read an iteration later, so its latency is spent
+  // classifying.  (All of this is warp-uniform.)
+  unsigned long long r_base = 0, n_base = 0;
+  int r_left = 0, n_left = 0;
+  bool n_pend = false, n_have = false;
+  unsigned long long claim_ret = 0;  // (lane 0's register)
   for (;;) {
-    if (claim_mask) {
-      const unsigned long long base = __shfl_sync(FULL, claim_base, claim_leader);
-      if (base + __popc(claim_mask) >= total) dry = true;
-      if ((claim_mask >> lane) & 1u) {
-        const unsigned long long kq = base + __popc(claim_mask & ((1u << lane) - 1u));
-        if (kq < total) {
-          // start the copy of the entry's record
-          const double* src = reinterpret_cast<const double*>(
-              &io.rec[KIND ? io.rec_cap - 1 - (long long)kq : (long long)kq]);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) cp_async8(col + (kColQ + i) * kLaneNT, src + i);
-          state = 1;
-        } else {
-          state = 0;
-        }
+    if (n_pend) {
+      const unsigned long long base = __shfl_sync(FULL, claim_ret, 0);
+      n_pend = false;
+      if (base >= total) {
+        dry = true;
+      } else {
+        n_base = base;
+        n_left = (int)(total - base < (unsigned long long)kLaneClaim ? total - base : kLaneClaim);
+        n_have = true;
       }
-      claim_mask = 0;
+    }
+    if (r_left == 0 && n_have) {
+      r_base = n_base;
+      r_left = n_left;
+      n_have = false;
+    }
+    if (!dry && !n_pend && !n_have && r_left < kLaneClaim / 2) {
+      if (lane == 0) claim_ret = atomicAdd(&io.next[kind], (unsigned long long)kLaneClaim);
+      n_pend = true;
     }
     const unsigned need = __ballot_sync(FULL, state == 0);
-    if (need && !dry) {
-      claim_leader = __ffs(need) - 1;
-      if (lane == claim_leader) claim_base = atomicAdd(&io.next[KIND], (unsigned long long)__popc(need));
-      claim_mask = need;
-      if (state == 0) state = 4;  // (claimed, the entry index arrives next iteration)
+    if (need && r_left > 0) {
+      const int rank = __popc(need & ((1u << lane) - 1u));
+      const int take = __popc(need) < r_left ? __popc(need) : r_left;
+      if (state == 0 && rank < take) {
+        // start the copy of the entry's record
+        const unsigned long long kq = r_base + rank;
+        const double* src = reinterpret_cast<const double*>(
+            &io.rec[kind ? io.rec_cap - 1 - (long long)kq : (long long)kq]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cp_async8(col + (kColQ + i) * kLaneNT, src + i);
+        state = 1;
+      }
+      r_base += take;
+      r_left -= take;
     }
-    if (!__any_sync(FULL, state != 0)) break;
-    if (state == 4) continue;
+    if (!__any_sync(FULL, state != 0)) {
+      // nothing in flight: done once the queue is known empty
+      if (dry && r_left == 0 && !n_have && !n_pend) break;
+      continue;
+    }
+    if (state == 0) continue;
     if (state == 1) {
       // the record has landed (one iteration later): copy the coordinates
       // and the per-query parameters
@@ -349,7 +376,8 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     b.u0 = (double)((pk >> nv) & ((1ull << nu) - 1ull)) * wu; b.u1 = b.u0 + wu;
     b.v0 = (double)(pk & ((1ull << nv) - 1ull)) * wv; b.v1 = b.v0 + wv;
     double wb;
-    const int cls = classify_full<KIND>(P, b, eps, sep, wb);
+    const int cls = kind == 0 ? classify_full<0>(P, b, eps, sep, wb)
+                              : classify_full<1>(P, b, eps, sep, wb);
     ++C;
     const bool disj = cls == kDisjoint;
     const bool budget = C >= mc;
@@ -388,7 +416,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     const unsigned long long lo = ((pk >> pos) << (pos + 1)) | (pk & ((1ull << pos) - 1ull));
     const unsigned long long hi = lo | (1ull << pos);
     bool push_hi = true;
-    if (KIND == 0) {
+    if (kind == 0) {
       const bool hu = 0.5 * (b.u0 + b.u1) + b.v0 <= 1.0;
       const bool hv = b.u0 + 0.5 * (b.v0 + b.v1) <= 1.0;
       push_hi = sd == 0 ? true : (sd == 1 ? hu : hv);
@@ -424,7 +452,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
         lane_write(a, col, kColDr, C, 0);
       } else {
         const Box z = {0, 0, 0, 0, 0, 0};
-        write_result(a, __double_as_longlong(col[kColQ * kLaneNT]), kFree, z, 0.0, C, 0, 0);
+        lane_emit(a, __double_as_longlong(col[kColQ * kLaneNT]), kFree, z, 0.0, C, 0, 0);
       }
       outcome = 1;
     }
@@ -516,7 +544,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       state = 0;
     }
   }
-  lane_flush<KIND>(io, st);
+  lane_flush(io, st, kind);
 }
 
 __global__ void __launch_bounds__(kLaneNT, TCCD_NMINB) lane_kernel(Args a, LaneIO io) {
@@ -529,10 +557,7 @@ __global__ void __launch_bounds__(kLaneNT, TCCD_NMINB) lane_kernel(Args a, LaneI
   // their queues; a warp whose queue runs dry moves to the other one
   const long long gw = gt >> 5, nw = (long long)gridDim.x * (kLaneNT / 32);
   int kind = (nvf + nee) > 0 && (unsigned long long)gw * (nvf + nee) < nee * (unsigned long long)nw;
-  for (int pass = 0; pass < 2; ++pass, kind ^= 1) {
-    if (kind == 0) lane_loop<0>(a, io, col, lb);
-    else lane_loop<1>(a, io, col, lb);
-  }
+  for (int pass = 0; pass < 2; ++pass, kind ^= 1) lane_loop(a, io, col, lb, kind);
 }
 
 }  // namespace tccd
