@@ -52,11 +52,23 @@ def _staging_buffer(device: torch.device, nbytes: int) -> list:
         if buf.numel() >= nbytes and (ev is None or (ev is not _BUSY and ev.query())):
             slot[1] = _BUSY
             return slot
+    # large batches: at most a few buffers in flight (each is the whole
+    # batch's points); past that, wait for the oldest solve to release one
+    cap = 16 if nbytes <= (256 << 20) else 3
+    fits = [sl for sl in slots if sl[0].numel() >= nbytes and sl[1] is not _BUSY]
+    if len(slots) >= cap and fits:
+        slot = fits[0]
+        if slot[1] is not None:
+            slot[1].synchronize()
+        slots.remove(slot)
+        slots.append(slot)  # (round robin: the next wait is for the next oldest)
+        slot[1] = _BUSY
+        return slot
     # (allocated on the copy stream that writes it: a block the caller's
     # stream freed a moment ago may still be read there)
     with torch.cuda.stream(copy_stream(device)):
         slot = [torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device), _BUSY]
-    if len(slots) < 16:
+    if len(slots) < cap:
         slots.append(slot)
     return slot
 
