@@ -541,6 +541,10 @@ long long giant_cap(long long mcmax) { return 2 * mcmax + 2; }
 #define TCCD_LANE_HAND (1LL << 21)
 #endif
 constexpr long long kLaneHandMax = TCCD_LANE_HAND;  // lane-tier handover records per chunk
+#ifndef TCCD_LANE_POOL
+#define TCCD_LANE_POOL (1LL << 26)
+#endif
+constexpr long long kLanePoolDefault = TCCD_LANE_POOL;  // lane-tier handover pool boxes per chunk
 
 struct Layout {
   size_t ctr, light_q, lq, lscratch, queue[3], hand[3], pbox[3], pflag[3], perm, light, medium,
@@ -563,7 +567,7 @@ Layout layout(long long n, long long mcmax, int giant_blocks, int sms, long long
   L.chunk = chunk;
   L.sub = sub;
   const long long pool = pool_boxes > 0 ? pool_boxes : kPoolDefault;
-  L.pool[0] = std::min(pool, chunk * kLaneArr);
+  L.pool[0] = std::min(pool_boxes > 0 ? pool_boxes : kLanePoolDefault, chunk * kLaneArr);
   L.hand0 = std::min(chunk, kLaneHandMax);
   L.pool[1] = std::min(pool, sub * 2 * LightCfg::QCAP);
   L.pool[2] = std::min(pool, sub * 2 * MediumCfg::QCAP);

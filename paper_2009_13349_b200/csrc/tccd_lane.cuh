@@ -46,7 +46,7 @@
 namespace tccd {
 
 #ifndef TCCD_KL
-#define TCCD_KL 64
+#define TCCD_KL 128
 #endif
 #ifndef TCCD_NNT
 #define TCCD_NNT 128
