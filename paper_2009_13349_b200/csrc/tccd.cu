@@ -465,14 +465,42 @@ __global__ void copy_counted_kernel(const unsigned char* src, unsigned char* dst
 // Admission order of the giant tier's queue: largest handed-over level
 // first (longest-processing-time-first, so the heaviest queries do not start
 // last and leave the other SMs idle).  Only a scheduling order: every query's
-// result is independent of it.  Queues above kOrderMax keep their order.
+// result is independent of it.  Queues up to kOrderMax are sorted exactly
+// (bitonic, one CTA); longer ones are ordered by a counting sort on the
+// level size's power of two (descending; arbitrary within a bucket), up to
+// the sub-chunk's capacity.
 constexpr int kOrderMax = 4096;
 __global__ void __launch_bounds__(1024) order_kernel(const Hand* hand,
                                                      const unsigned long long* count,
-                                                     unsigned int* perm) {
+                                                     unsigned int* perm, long long cap) {
   __shared__ unsigned long long key[kOrderMax];
+  __shared__ unsigned int bucket[33];
   const unsigned long long n = *count;
-  if (n < 2 || n > (unsigned long long)kOrderMax) return;
+  if (n < 2) return;
+  if (n > (unsigned long long)kOrderMax) {
+    if (n > (unsigned long long)cap) return;
+    // bucket b holds the entries with 2^(32-b-1) <= level boxes < 2^(32-b) (b = 32: no level)
+    auto bkt = [&](unsigned long long i) -> int {
+      const int h = hand[i].n;
+      return h > 0 ? __clz(h) : 32;
+    };
+    for (int i = threadIdx.x; i < 33; i += blockDim.x) bucket[i] = 0;
+    __syncthreads();
+    for (unsigned long long i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&bucket[bkt(i)], 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned int sum = 0;
+      for (int k = 0; k < 33; ++k) {
+        const unsigned int c = bucket[k];
+        bucket[k] = sum;
+        sum += c;
+      }
+    }
+    __syncthreads();
+    for (unsigned long long i = threadIdx.x; i < n; i += blockDim.x)
+      perm[atomicAdd(&bucket[bkt(i)], 1u)] = (unsigned int)i;
+    return;
+  }
   int P = 2;
   while (P < (int)n) P <<= 1;
   for (int i = threadIdx.x; i < P; i += blockDim.x) {
@@ -595,7 +623,7 @@ Layout layout(long long n, long long mcmax, int giant_blocks, int sms, long long
     L.pbox[k] = o; o += align256((size_t)L.pool[k] * sizeof(Box));
     L.pflag[k] = o; o += align256((size_t)L.pool[k]);
   }
-  L.perm = o; o += align256((size_t)kOrderMax * 4);
+  L.perm = o; o += align256((size_t)sub * 4);
   L.light = o; o += L.light_b * (size_t)L.light_blocks * groups_per_cta<LightCfg>();
   L.medium = o; o += L.medium_b * (size_t)L.medium_blocks * groups_per_cta<MediumCfg>();
   L.giant = o; o += L.giant_b * (size_t)L.giant_blocks;
@@ -794,7 +822,7 @@ int tccd_solve_batch(const tccd_batch* b_in, void* stream) {
                   : (tier == 0 ? (lanes ? kLaneArr : 1)
                                : 2 * (tier == 1 ? LightCfg::QCAP : MediumCfg::QCAP));
     io.in_perm = tier == 2 && !a.heavy_only ? (const unsigned int*)(ws + L.perm) : nullptr;
-    io.perm_max = kOrderMax;
+    io.perm_max = L.sub;
     io.out_hand = tier < 2 ? (Hand*)(ws + L.hand[tier + 1]) : nullptr;
     io.out_pbox = tier < 2 ? (Box*)(ws + L.pbox[tier + 1]) : nullptr;
     io.out_pflag = tier < 2 ? (uint8_t*)(ws + L.pflag[tier + 1]) : nullptr;
@@ -891,7 +919,7 @@ int tccd_solve_batch(const tccd_batch* b_in, void* stream) {
         ++launches;
         if (mark(TCCD_STAGE_MEDIUM) != cudaSuccess) return TCCD_E_CUDA;
         order_kernel<<<1, 1024, 0, st>>>((const Hand*)(ws + L.hand[2]), &ctr->q_count[2],
-                                         (unsigned int*)(ws + L.perm));
+                                         (unsigned int*)(ws + L.perm), L.sub);
         ++launches;
         if (cudaGetLastError() != cudaSuccess) return TCCD_E_CUDA;
       }
