@@ -173,7 +173,11 @@ __device__ __forceinline__ void load_params(const Args& a, long long q, QueryPar
 
 }  // namespace tccd
 
+#ifdef TCCD_LANE_BOXWISE
+#include "tccd_lane_boxwise.cuh"  // (round-2 first lane tier: one box per iteration; A/B timing only)
+#else
 #include "tccd_lane.cuh"
+#endif
 
 namespace tccd {
 
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long
           survive = true;
           int ex;
           // lane tier: dyadic t_max (lattice boxes) and tame coordinates
-          if (lq && qp.tame && frexp(qp.t_max, &ex) == 0.5) {
+          if (lq && qp.tame && frexp(qp.t_max, &ex) == 0.5 && qp.t_max >= 0x1p-900) {
             lane_kind = qp.kind;
             lr.q = q;
             lr.wb = wb;
@@ -645,6 +649,17 @@ int configure() {
   return TCCD_OK;
 }
 
+int configure_lane() {
+  static bool done[256] = {};
+  const int dev = current_device();
+  if (dev >= 0 && dev < 256 && done[dev]) return TCCD_OK;
+  if (cudaFuncSetAttribute(lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kLaneSmemBytes) != cudaSuccess)
+    return TCCD_E_CUDA;
+  if (dev >= 0 && dev < 256) done[dev] = true;
+  return TCCD_OK;
+}
+
 template <class Cfg>
 int launch_tier(const Args& a, const TierIO& io, int blocks, cudaStream_t st) {
   if (configure<Cfg>() != TCCD_OK) return TCCD_E_CUDA;
@@ -894,7 +909,8 @@ int tccd_solve_batch(const tccd_batch* b_in, void* stream) {
     }
     if (mark(TCCD_STAGE_PROLOGUE) != cudaSuccess) return TCCD_E_CUDA;
     if (lanes) {
-      lane_kernel<<<L.lane_blocks, kLaneNT, 0, st>>>(a, lio);
+      if (configure_lane() != TCCD_OK) return TCCD_E_CUDA;
+      lane_kernel<<<L.lane_blocks, kLaneNT, kLaneSmemBytes, st>>>(a, lio);
       ++launches;
       if (cudaGetLastError() != cudaSuccess || mark(TCCD_STAGE_LANE) != cudaSuccess)
         return TCCD_E_CUDA;

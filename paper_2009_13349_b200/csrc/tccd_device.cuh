@@ -187,6 +187,63 @@ __device__ __forceinline__ int classify_full(PtrT P, const Box& b, EpsT eps, dou
   return disjoint ? kDisjoint : (contained ? kContained : kIntersects);
 }
 
+// classify_full of two boxes at once (the two children of a refined box):
+// two independent evaluations a thread interleaves axis by axis (the lane
+// tier classifies children when their parent is refined).  Each box sees
+// exactly classify_full's operations.
+template <int KIND, typename PtrT, typename EpsT>
+__device__ __forceinline__ void classify_pair(PtrT P, const Box& a, const Box& b, EpsT eps,
+                                              double sep, int& cls_a, double& wb_a, int& cls_b,
+                                              double& wb_b) {
+#ifdef TCCD_PAIR_HOIST
+  const CornerWeights wa = corner_weights(a), wb = corner_weights(b);
+  const double a_omt0 = 1.0 - a.t0, a_omt1 = 1.0 - a.t1;
+  const double b_omt0 = 1.0 - b.t0, b_omt1 = 1.0 - b.t1;
+#endif
+  bool dis_a = false, con_a = true, dis_b = false, con_b = true;
+  double wid_a = 0.0, wid_b = 0.0;
+#ifdef TCCD_FULL_UNROLL
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+  for (int ax = 0; ax < 3; ++ax) {
+    double mna, mxa, mnb, mxb;
+#ifndef TCCD_PAIR_HOIST
+    // the corner weights are recomputed per axis (10 DADD per box) instead
+    // of held in 2 x 14 double registers across the axis loop: the boxes
+    // are made opaque to the compiler's loop-invariant hoisting
+    Box a2 = a, b2 = b;
+    asm volatile("" : "+d"(a2.t0), "+d"(a2.t1), "+d"(a2.u0), "+d"(a2.u1), "+d"(a2.v0), "+d"(a2.v1));
+    asm volatile("" : "+d"(b2.t0), "+d"(b2.t1), "+d"(b2.u0), "+d"(b2.u1), "+d"(b2.v0), "+d"(b2.v1));
+    {
+      const CornerWeights wa = corner_weights(a2);
+      hull_axis<KIND, true>(P, ax, a2.t0, 1.0 - a2.t0, a2.t1, 1.0 - a2.t1, wa, mna, mxa);
+    }
+    {
+      const CornerWeights wb = corner_weights(b2);
+      hull_axis<KIND, true>(P, ax, b2.t0, 1.0 - b2.t0, b2.t1, 1.0 - b2.t1, wb, mnb, mxb);
+    }
+#else
+    hull_axis<KIND, true>(P, ax, a.t0, a_omt0, a.t1, a_omt1, wa, mna, mxa);
+    hull_axis<KIND, true>(P, ax, b.t0, b_omt0, b.t1, b_omt1, wb, mnb, mxb);
+#endif
+    const double e = eps[ax];
+    const double loa = mna - sep, hia = mxa + sep, lob = mnb - sep, hib = mxb + sep;
+    dis_a |= loa > e || hia < -e;
+    dis_b |= lob > e || hib < -e;
+    con_a &= loa >= -e && hia <= e;
+    con_b &= lob >= -e && hib <= e;
+    const double da = mxa - mna, db = mxb - mnb;
+    wid_a = da > wid_a ? da : wid_a;
+    wid_b = db > wid_b ? db : wid_b;
+  }
+  wb_a = dis_a ? 0.0 : wid_a;
+  wb_b = dis_b ? 0.0 : wid_b;
+  cls_a = dis_a ? kDisjoint : (con_a ? kContained : kIntersects);
+  cls_b = dis_b ? kDisjoint : (con_b ? kContained : kIntersects);
+}
+
 template <typename PtrT>
 __device__ __forceinline__ int classify(PtrT P, int kind, const Box& b, const double* eps,
                                         double sep, double& wb, bool tame = false) {

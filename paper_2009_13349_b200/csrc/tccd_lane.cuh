@@ -1,4 +1,4 @@
-// Lane tier: one query per thread, one box check per loop iteration.
+// Lane tier: one query per thread, one REFINING box per loop iteration.
 //
 // Most queries of simulation-shaped batches (BASELINE config 3) stay shallow:
 // their levels hold a handful of boxes (p50 4, p99 54)
@@ -6,11 +6,31 @@
 // level per round pays its per-round bookkeeping (barriers, scans, layout)
 // for very few boxes.  Here every thread runs the reference's state machine
 // (ccdkit._kernel.solve_kernel, pkg/src/ccdkit/_kernel.py:173-324) for one
-// query at a time, box by box in the reference's visiting order, and takes
-// the next query from a shared queue as soon as its query ends, so every
-// lane classifies one box per iteration whatever depth its query has.  A
-// warp works on one query kind at a time (classify() never diverges on the
-// kind).
+// query at a time and takes the next query from a shared queue as soon as its
+// query ends.  A warp works on one query kind at a time (the classification
+// never diverges on the kind).
+//
+// Children are classified when their parent is refined.  Half of all boxes
+// checked are disjoint (config 3: 49%), and a disjoint box does nothing in
+// the reference but count as a check (_kernel.py:186-199, budget aside).  So
+// an iteration takes one non-disjoint box of the current level in the
+// reference's visiting order, runs the state machine's events for it (first
+// box of its level, accept, drop record: _kernel.py:201-258), and, when it
+// refines, classifies BOTH children at once -- two independent evaluations a
+// thread interleaves -- and stores only the non-disjoint ones, with their
+// class and hull width, for the next level.  Disjoint children are counted,
+// never stored or visited: per level the lane keeps the number of all
+// children (the checks the reference spends on the level) and the visiting
+// rank, among all of them, of the first non-disjoint one (the check count of
+// a query that ends there, _kernel.py:243-252).  The per-box bookkeeping
+// runs once per refining box instead of once per box.  What is classified
+// beyond the reference's path is the rest of a level whose first non-disjoint
+// box ends the query (config 3: 2% of the checks); the results do not depend
+// on it (classification is a pure function of the box).
+//
+// The check budget: a level whose boxes could reach m_I is never processed
+// here (the query restarts in the light tier, which replays budget returns
+// exactly), so the lane's state machine has no budget events.
 //
 // Boxes as lattice indices.  With a dyadic t_max every box of level L is a
 // cell of the lattice with per-dimension split counts (nt, nu, nv), nt + nu
@@ -22,25 +42,30 @@
 // along one dimension (same widths, same kappas), so its children are
 // visited in the order the reference's stable t_lo sort gives them: push
 // order after a u / v split; after a t split, per run of equal parent t_lo,
-// all lower children then all upper children.  Children are stored in push
-// order (lower, upper, lower, upper, ...) with the length of each parent
-// run's segment, and a t-split level's successor is visited segment by
-// segment, even positions first: no box is ever moved.
+// all lower children then all upper children.  A level array is filled from
+// both ends: entries that keep their parent's t_lo (lower children, both
+// children of u / v splits) upward from the bottom, upper children of t
+// splits downward from the top, with one (count, count) segment per run of
+// parents; the next level is visited segment by segment, bottom part then
+// top part: no entry is ever moved.
 //
-// Latency: the word of the next box is loaded while the current box is
-// classified; a lane that takes a new query copies its 64-byte record
-// (index, filters, kappas) and then the query's coordinates and parameters
-// into its shared-memory column with cp.async, one iteration apart, and
-// starts on it the iteration after, so neither stalls the warp.
+// Latency: the entry of the next box is loaded while the current box's
+// children are classified; a lane that takes a new query copies its 64-byte
+// record (index, filters, kappas) and then the query's coordinates and
+// parameters into its shared-memory column with cp.async, one iteration
+// apart, and starts on it the iteration after, so neither stalls the warp.
 //
 // A query leaves this tier when its next level has more than kLaneCap
-// boxes (the level arrays hold 2 kLaneCap, so a level of at most kLaneCap
-// boxes always has room for its children): that level goes to the light
-// tier's handover pool, in visiting order with its run heads, with the
-// check count and first / drop records, and the light tier resumes the
-// query there.  If the handover pool is full, or the lattice would exceed
-// its index range, the query restarts from its root in the light tier
-// instead (exact: classification is a pure function of the box).
+// non-disjoint boxes (the level arrays hold 2 kLaneCap entries, so the
+// children of a level of at most kLaneCap always fit): that level's
+// non-disjoint boxes go to the light tier's handover pool, in visiting order
+// with their run heads, with the check count up to that level plus the
+// level's disjoint boxes, and the first / drop records; the light tier
+// resumes the query there and classifies exactly the boxes the reference
+// still has to count.  (Only when the level's first box is not one that ends
+// the query: that one the lane finishes itself.)  If the handover pool is
+// full, the budget is near, or the lattice would exceed its index range, the
+// query restarts from its root in the light tier instead.
 #pragma once
 
 namespace tccd {
@@ -54,7 +79,7 @@ namespace tccd {
 #ifndef TCCD_NMINB
 #define TCCD_NMINB 4
 #endif
-constexpr int kLaneCap = TCCD_KL;  // largest level a lane processes
+constexpr int kLaneCap = TCCD_KL;  // largest level (non-disjoint boxes) a lane processes
 constexpr int kLaneArr = 2 * kLaneCap;  // level array capacity: its children always fit
 constexpr int kLaneNT = TCCD_NNT;  // threads per CTA
 constexpr int kLaneMaxSplits = 52;  // per dimension: midpoints stay exact (indices < 2^53)
@@ -67,10 +92,17 @@ constexpr int kLaneTailChecks = TCCD_LANE_TAIL;  // (tail handover threshold)
 #define TCCD_LANE_CLAIM 32
 #endif
 constexpr int kLaneClaim = TCCD_LANE_CLAIM;  // queue entries a warp claims at once
-// per-lane global scratch: two level arrays of words and two segment tables
-// (a level's segments: at most one per refining box of the level before)
-constexpr int kLaneSeg = kLaneCap;
-constexpr int kLaneScratchWords = 2 * kLaneArr + kLaneSeg;  // (segment tables: 2 x u32 per word)
+
+// A stored (non-disjoint) box: its lattice word and its hull width, negated
+// (sign bit) when the box is contained in the filter box
+struct alignas(16) LaneEnt {
+  unsigned long long pk;
+  double w;
+};
+// per-lane global scratch: two level arrays and two segment tables (a
+// level's segments are non-empty, so at most one per entry)
+constexpr int kLaneSeg = kLaneArr;
+constexpr int kLaneScratchWords = 2 * kLaneArr * 2 + kLaneSeg;  // (segment tables: 2 x u32 per word)
 
 // A query queued for the lane tier by the prologue: its root box is
 // non-disjoint and refined (one check done); its filters and kappas.
@@ -83,11 +115,12 @@ struct LaneRec {
 static_assert(sizeof(LaneRec) == 64, "LaneRec layout");
 // shared-memory column of one lane: the 24 coordinates, the LaneRec words,
 // the per-query parameters, and the first / drop records (lattice word,
-// codomain width, split counts | level << 24) -- read only when a query
-// ends, so they do not hold registers
-constexpr int kLaneCol = 42;
+// codomain width, split counts | level << 24) and the drop record's t_lo --
+// read only when a box is accepted, so they do not hold registers
+constexpr int kLaneCol = 45;
 constexpr int kColQ = 24, kColWb = 25, kColEps = 26, kColKap = 29, kColSep = 32, kColDelta = 33,
-              kColTmax = 34, kColMc = 35, kColFr = 36, kColDr = 39;
+              kColTmax = 34, kColMc = 35, kColFr = 36, kColDr = 39, kColDrT0 = 42,
+              kColF0 = 43 /* [2]: the next level's first entry */;
 
 struct LaneIO {
   const LaneRec* rec;             // vertex-face entries from the front, edge-edge from the back
@@ -97,7 +130,7 @@ struct LaneIO {
   unsigned long long* scratch;      // [grid threads][kLaneScratchWords]
   Pre* out;                         // light-tier queue (evicted queries go there)
   unsigned long long* out_count;
-  unsigned long long* stats;        // [8] see Counters::lane
+  unsigned long long* stats;        // [10] see Counters::lane
   // handover to the light tier: state records and the pool of level boxes
   Hand* hand;
   long long hand_cap;
@@ -171,118 +204,136 @@ __device__ __forceinline__ int lane_record_level(const double* col, int at) {
   return (int)__double_as_longlong(col[(at + 2) * kLaneNT]) >> 24;
 }
 
-__device__ __forceinline__ void lane_emit(const Args& a, long long q, uint8_t status, Box b,
-                                       double codom, long long checks, int early, int level) {
-  write_result(a, q, status, b, codom, checks, early, level);
-}
-
 // the result of a query that ends on the record at column offset `at`
 __device__ __forceinline__ void lane_write(const Args& a, const double* col, int at,
-                                           long long checks, int early) {
+                                           long long checks) {
   const long long q = __double_as_longlong(col[kColQ * kLaneNT]);
   const double t_max = col[kColTmax * kLaneNT];
-  lane_emit(a, q, kHit, lane_record_box(col, at, t_max), col[(at + 1) * kLaneNT], checks, early,
-            lane_record_level(col, at));
+  write_result(a, q, kHit, lane_record_box(col, at, t_max), col[(at + 1) * kLaneNT], checks, 0,
+               lane_record_level(col, at));
 }
 
-struct LaneStats {
-  unsigned int checks = 0, done = 0, evicted = 0, wasted = 0, handed = 0;
-};
+// per-thread 32-bit slots in shared memory: the pass's counters (touched when
+// a query ends) and the rank bookkeeping of a level's first box (touched
+// once per level) -- none of it holds registers
+constexpr int kLaneInt = 9;
+constexpr int kIntCls = 0, kIntChecks = 1, kIntDone = 2, kIntEvicted = 3, kIntWasted = 4,
+              kIntHanded = 5, kIntPf = 6 /* [2]: by level parity */, kIntRk = 8;
 
-// add this warp's counters of one pass to the tier's (warp-reduced)
-__device__ __forceinline__ void lane_flush(const LaneIO& io, const LaneStats& st, int kind) {
-  // (classifications: the checks on the reference's path + the ones repeated)
-  const unsigned int v[6] = {st.checks + st.wasted, st.checks, st.done, st.evicted, st.wasted,
-                             st.handed};
+// add this warp's counters of one pass to the tier's (warp-reduced), and
+// clear them
+__device__ __forceinline__ void lane_flush(const LaneIO& io, unsigned* si, int kind) {
+  // (classifications: every child evaluated, on the reference's path or not)
   const int slot[6] = {kind, 2 + kind, 4 + kind, 6, 7, 8};
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
-    unsigned long long x = v[i];
+    unsigned long long x = si[i * kLaneNT];
+    si[i * kLaneNT] = 0u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     if ((threadIdx.x & 31) == 0 && x) atomicAdd(&io.stats[slot[i]], x);
   }
 }
 
+// 2^(x - 1023) from its exponent field (0 < x < 2047): exact, two integer
+// instructions, so a level's widths need no registers of their own
+__device__ __forceinline__ double lane_pow2(int x) { return __hiloint2double(x << 20, 0); }
+
 // One kind's queue (kind is warp-uniform; only the classification is
 // specialized on it, so the loop's code exists once).
 __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, double* col,
-                                          unsigned long long* lb, const int kind) {
-  LaneStats st;
+                                          unsigned* si_, unsigned* wq, unsigned long long* lb,
+                                          const int kind) {
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const ColP<kLaneNT> P{col};
   const ColP<kLaneNT> eps{col + kColEps * kLaneNT};
   const ColP<kLaneNT> kap{col + kColKap * kLaneNT};
-  unsigned int* const segs = reinterpret_cast<unsigned int*>(lb + 2 * kLaneArr);  // [2][kLaneSeg]
-  const unsigned long long total = io.count[kind];
+  LaneEnt* const ent = reinterpret_cast<LaneEnt*>(lb);  // [2][kLaneArr]
+  unsigned int* const segs = reinterpret_cast<unsigned int*>(lb + 2 * kLaneArr * 2);  // [2][kLaneSeg]
   bool dry = false;  // (warp-uniform) this kind's queue is empty
   int state = 0;     // 0 idle, 1 record in flight, 2 coordinates in flight, 3 active
-  // query
-  int mc = 0, C = 0;  // (a lane query stays far below 2^31 checks: <= 62 levels of <= 64 boxes)
-  double sep = 0, delta = 0;
-  // level: split counts and widths of its boxes, its split dimension
-  int L = 0, nt = 0, nu = 0, nv = 0, sd = 0;
-  double wt = 1, wu = 1, wv = 1;
-  int cb = 0;        // current level array: lb + cb (the next one: lb + (cb ^ kLaneArr))
-  int sgb = 0;       // current segment table: segs + sgb (the next one: segs + (sgb ^ kLaneSeg))
+  // checks before the current level; the level's boxes (all of them, the
+  // checks the reference spends on it).  (A lane query stays far below 2^31
+  // checks: <= 62 levels of <= 4 kLaneCap boxes.)  The visiting rank, among
+  // all of them, of the level's first non-disjoint box: si_[kIntPf + parity].
+  int Cb = 0, nall = 0;
+  // level: split counts of its boxes (widths 2^(xt - nt - 1023), 2^-nu,
+  // 2^-nv; xt: t_max's exponent field), its split dimension
+  int nt = 0, nu = 0, nv = 0, xt = 0, sd = 0;
+  // current level array ent + cb and segment table segs + cb (the next
+  // ones: cb ^ kLaneArr; kLaneSeg == kLaneArr)
+  int cb = 0;
   int ncur = 0, k = 0;
-  // visiting order of the current level: identity, or (after a t split)
-  // segment by segment, even positions first
-  bool ilv = false;
-  int seg_start = 0, seg_m = 0, seg_k = 0, seg_i = 0, seg_mn = 0, nseg = 0;
-  unsigned long long pk = 0, pk_next = 0;
-  // next level: children written, segments closed, the current run (t split)
-  int nn = 0, nsn = 0, run_m = 0, seg0 = 0;
-  unsigned long long run = ~0ull, nxt0 = 0;
-  bool col_lvl = false;  // this level has had a non-disjoint box (last_colliding_level)
-  double fr_t0 = 0, dr_t0 = 0;  // t_lo of the first / drop records (the rest: in the column)
-  bool hf = false, hd = false;
+  // visiting order of the current level: per segment the bottom part upward,
+  // then the top part downward.  rAB: entries left in the segment after the
+  // prefetched one (bottom | top << 16), pa: the next bottom position (the
+  // next top position follows from k), sn: the next segment.
+  unsigned rAB = 0, sn = 0;
+  int pa = 0, si = 0, nseg = 0;
+  unsigned long long pk = 0;
+  double w = 0;
+  ulonglong2 nx = make_ulonglong2(0ull, 0ull);  // the next entry (word, width bits)
+  // next level: entries (bottom | top << 16), segments closed, the current
+  // run of parents (t split: equal t_lo; else the whole level): its entries,
+  // its refining parents, the children of the runs before it
+  unsigned nAB = 0, runAB = 0;
+  int nsn = 0, run_m = 0, run_base = 0, nall_next = 0;
+  unsigned long long run = ~0ull;
+  unsigned seg0 = 0, seg1 = 0;  // (the next level's first two segments)
+  bool hd = false;
+  static_assert(kLaneSeg == kLaneArr, "one parity offset for both tables");
 
   // The warp claims queue entries kLaneClaim at a time (one atomic on the
   // kind's counter per range, not per query) and hands them to its idle
   // lanes; the next range is claimed while the current one still lasts, and
   // the atomic's result is read an iteration later, so its latency is spent
-  // classifying.  (All of this is warp-uniform.)
-  unsigned long long r_base = 0, n_base = 0;
-  int r_left = 0, n_left = 0;
+  // classifying.  (All of this is warp-uniform; the ranges live in the
+  // warp's shared-memory words wq: [0] current base, [1] next base, [2] next
+  // length, [3] the queue's length.)
+  wq[3] = (unsigned)io.count[kind];  // (a chunk's queue: <= 2^26 entries)
+  int r_left = 0;
   bool n_pend = false, n_have = false;
-  unsigned long long claim_ret = 0;  // (lane 0's register)
+  unsigned claim_ret = 0;  // (lane 0's register)
   for (;;) {
     if (n_pend) {
-      const unsigned long long base = __shfl_sync(FULL, claim_ret, 0);
+      const unsigned base = __shfl_sync(FULL, claim_ret, 0);
+      const unsigned total = wq[3];
       n_pend = false;
       if (base >= total) {
         dry = true;
       } else {
-        n_base = base;
-        n_left = (int)(total - base < (unsigned long long)kLaneClaim ? total - base : kLaneClaim);
+        wq[1] = base;
+        wq[2] = total - base < (unsigned)kLaneClaim ? total - base : (unsigned)kLaneClaim;
         n_have = true;
       }
     }
     if (r_left == 0 && n_have) {
-      r_base = n_base;
-      r_left = n_left;
+      wq[0] = wq[1];
+      r_left = (int)wq[2];
       n_have = false;
     }
     if (!dry && !n_pend && !n_have && r_left < kLaneClaim / 2) {
-      if (lane == 0) claim_ret = atomicAdd(&io.next[kind], (unsigned long long)kLaneClaim);
+      // (the counter's low word: at most the queue's length + warps * kLaneClaim)
+      if (lane == 0) claim_ret = (unsigned)atomicAdd(&io.next[kind], (unsigned long long)kLaneClaim);
       n_pend = true;
     }
     const unsigned need = __ballot_sync(FULL, state == 0);
     if (need && r_left > 0) {
       const int rank = __popc(need & ((1u << lane) - 1u));
       const int take = __popc(need) < r_left ? __popc(need) : r_left;
+      const unsigned r_base = wq[0];
       if (state == 0 && rank < take) {
         // start the copy of the entry's record
-        const unsigned long long kq = r_base + rank;
+        const unsigned kq = r_base + rank;
         const double* src = reinterpret_cast<const double*>(
             &io.rec[kind ? io.rec_cap - 1 - (long long)kq : (long long)kq]);
 #pragma unroll
         for (int i = 0; i < 8; ++i) cp_async8(col + (kColQ + i) * kLaneNT, src + i);
         state = 1;
       }
-      r_base += take;
+      __syncwarp();
+      wq[0] = r_base + take;
       r_left -= take;
     }
     if (!__any_sync(FULL, state != 0)) {
@@ -312,252 +363,319 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     }
     if (state == 2) {
       cp_async_wait_all();
-      {
-        const long long m = __double_as_longlong(col[kColMc * kLaneNT]);
-        mc = m < 0x7fffffffLL ? (int)m : 0x7fffffff;
-      }
-      sep = col[kColSep * kLaneNT];
-      delta = col[kColDelta * kLaneNT];
-      const double t_max = col[kColTmax * kLaneNT];
-      // the root (level 0, one check, the prologue's) is the first record
-      // and was refined: level 1 = its two children (never clipped: a root
-      // child's lower corner is 0)
-      lane_record(col, kColFr, 0ull, col[kColWb * kLaneNT], 0);
-      fr_t0 = 0.0;
-      hf = true; hd = false;
-      C = 1;
+      // level 0: the root, classified by the prologue (non-disjoint, to be
+      // refined: one check, rank 0); this lane's first iteration records it
+      // as the level's first box and classifies its two children
+      Cb = 0; nall = 1;
+      si_[kIntPf * kLaneNT] = 0u;
       nt = nu = nv = 0;
-      wt = t_max; wu = 1.0; wv = 1.0;
-      const int s0 = lane_split_dim(wt, wu, wv, kap);
-      if (s0 == 0) { nt = 1; wt *= 0.5; } else if (s0 == 1) { nu = 1; wu *= 0.5; } else { nv = 1; wv *= 0.5; }
-      cb = 0; sgb = 0;
-      lb[0] = 0ull;
-      lb[1] = 1ull;
-      ncur = 2; k = 0; L = 1;
-      // (a t split of the root leaves one run of one parent: order 0, 1 either way)
-      ilv = false; seg_start = 0; seg_m = 0; seg_k = 0; seg_i = 0; seg_mn = 0; nseg = 0;
-      pk = 0; pk_next = 1;
-      nn = 0; nsn = 0; run_m = 0; seg0 = 0; run = ~0ull; nxt0 = 0;
-      col_lvl = false;
-      sd = lane_split_dim(wt, wu, wv, kap);
+      // (t_max is a power of two in the normal range: the prologue's test)
+      xt = (int)(__double2hiint(col[kColTmax * kLaneNT]) >> 20);
+      sd = lane_split_dim(lane_pow2(xt), 1.0, 1.0, kap);
+      cb = 0;
+      ncur = 1; k = 0;
+      rAB = 0; pa = 0; si = 0; nseg = 1; sn = 0;
+      pk = 0; w = col[kColWb * kLaneNT];
+      nAB = runAB = 0;
+      nsn = run_m = run_base = nall_next = 0;
+      run = ~0ull;
+      hd = false;
       state = 3;
     }
     if (state != 3) continue;  // (idle: this kind's queue ran dry)
 
-    // ---- one box of the current level, in visiting order.  The bookkeeping
-    // is written as selects and predicated stores, so the lanes of a warp --
-    // each somewhere else in its own query -- run it together; only the
-    // writes of a finished query branch.
-    unsigned long long* const cur = lb + cb;
-    unsigned long long* const nxt = lb + (cb ^ kLaneArr);
-    unsigned int* const snx = segs + (sgb ^ kLaneSeg);
-    // the next box of this level: its word is loaded now, used next iteration
+    // ---- one non-disjoint box of the current level, in visiting order.  The
+    // bookkeeping is written as selects and predicated stores, so the lanes
+    // of a warp -- each somewhere else in its own query -- run it together;
+    // only the rare events (an accepted box, a finished query) branch.
+    LaneEnt* const cur = ent + cb;
+    LaneEnt* const nxt = ent + (cb ^ kLaneArr);
+    unsigned int* const snx = segs + (cb ^ kLaneArr);
+    const int par = cb ? 1 : 0;
+    // the next entry of this level: loaded now, used next iteration
     const bool more = k + 1 < ncur;
-    const bool n_newseg = ilv && seg_k + 1 == 2 * seg_m;
-    const int n_start = n_newseg ? seg_start + 2 * seg_m : seg_start;
-    const int n_m = n_newseg ? seg_mn : seg_m;
-    const int n_k = n_newseg ? 0 : seg_k + 1;
-    const int n_i = seg_i + (n_newseg ? 1 : 0);
-    const int pos1 = !ilv ? k + 1 : (n_k < n_m ? n_start + 2 * n_k : n_start + 2 * (n_k - n_m) + 1);
-    if (more) pk_next = cur[pos1];
+    {
+      const bool newseg = rAB == 0;
+      rAB = newseg ? sn : rAB;
+      si += newseg ? 1 : 0;
+      if (more && newseg && si + 1 < nseg) sn = segs[cb + si + 1];
+      const bool useA = (rAB & 0xffffu) != 0;
+      const int posn = useA ? pa : kLaneArr - 2 - k + pa;
+      pa += useA ? 1 : 0;
+      rAB -= useA ? 1u : 0x10000u;
+      // (loaded unconditionally -- a level's last entry re-reads slot 0 --
+      // and straight into the registers that carry it to the next
+      // iteration: a predicated load went through temporaries that were
+      // copied, and waited for, right behind it)
+      nx = *reinterpret_cast<const ulonglong2*>(cur + (more ? posn : 0));
+    }
+    // closing a segment of the next level; its first one fixes the level's
+    // first box: the first bottom entry if it has one (kIntRk: its rank),
+    // else its first top entry (kIntRk: the children before the run plus its
+    // parent's index; the run's lower children, one per refining parent,
+    // come before it)
+    auto close_segment = [&](bool close) {
+      if (close) snx[nsn] = runAB;
+      if (close && nsn == 0) {
+        seg0 = runAB;
+        si_[(kIntPf + (par ^ 1)) * kLaneNT] =
+            si_[kIntRk * kLaneNT] + ((runAB & 0xffffu) ? 0u : (unsigned)run_m);
+      }
+      seg1 = close && nsn == 1 ? runAB : seg1;
+      nsn += close ? 1 : 0;
+    };
     const int suv = nu + nv;
     const unsigned long long ti = pk >> suv;
     // a t-split level: a new run of equal t_lo closes the previous run's
-    // segment of the next level
+    // segment of the next level (if it has entries)
     const bool new_run = sd == 0 && ti != run;
-    const bool close_run = new_run && run_m > 0;
-    if (close_run) snx[nsn] = (unsigned)run_m;
-    seg0 = close_run && nsn == 0 ? run_m : seg0;
-    nsn += close_run ? 1 : 0;
+    close_segment(new_run && runAB != 0);
+    run_base += new_run ? 2 * run_m : 0;
     run_m = new_run ? 0 : run_m;
+    runAB = new_run ? 0u : runAB;
     run = sd == 0 ? ti : run;
-    Box b;
-    b.t0 = (double)ti * wt; b.t1 = b.t0 + wt;
-    b.u0 = (double)((pk >> nv) & ((1ull << nu) - 1ull)) * wu; b.u1 = b.u0 + wu;
-    b.v0 = (double)(pk & ((1ull << nv) - 1ull)) * wv; b.v1 = b.v0 + wv;
-    double wb;
-    const int cls = kind == 0 ? classify_full<0>(P, b, eps, sep, wb)
-                              : classify_full<1>(P, b, eps, sep, wb);
-    ++C;
-    const bool disj = cls == kDisjoint;
-    const bool budget = C >= mc;
-    const bool accept = !disj && (wb < delta || cls == kContained);  // (:215)
-    // first colliding box of this level (:201-206)
-    const int meta = nt | (nu << 8) | (nv << 16) | (L << 24);
-    const bool first = !disj && !col_lvl;
-    if (first) lane_record(col, kColFr, pk, wb, meta);
-    fr_t0 = first ? b.t0 : fr_t0;
-    hf = hf || first;
-    // the ways this box can end the query
-    const bool end_disj = disj && budget && (hd || more || nn > 0);   // (:188-199)
-    const bool end_budget = !disj && budget;                          // (:208-213)
-    const bool end_acc = accept && !budget && !col_lvl;               // (:243-252)
-    int outcome = 0;  // 0 continue, 1 ended (result written), 2 evict
-    if (end_disj || end_budget || end_acc) {
-      const bool use_drop = hd && (end_acc ? dr_t0 < b.t0
-                                           : (end_disj ? (!hf || dr_t0 < fr_t0) : dr_t0 < fr_t0));
-      // (an accepted first box of its level: the record just written is it)
-      lane_write(a, col, use_drop ? kColDr : kColFr, C, end_acc ? 0 : 1);
-      outcome = 1;
+    const double wt = lane_pow2(xt - nt), wu = lane_pow2(1023 - nu), wv = lane_pow2(1023 - nv);
+    const double t0 = (double)ti * wt;
+    const double u0 = (double)((pk >> nv) & ((1ull << nu) - 1ull)) * wu;
+    const double v0 = (double)(pk & ((1ull << nv) - 1ull)) * wv;
+    const bool first = k == 0;  // the first non-disjoint box of its level (:201-206)
+    // accepted: hull narrower than delta, or contained (sign bit) (:215)
+    const bool accept = fabs(w) < col[kColDelta * kLaneNT] || __double_as_longlong(w) < 0;
+    const int meta = nt | (nu << 8) | (nv << 16) | ((nt + suv) << 24);
+    if (first) lane_record(col, kColFr, pk, fabs(w), meta);
+    int outcome = 0;  // 0 continue, 1 ended (result written), 2 restart, 3 hand over
+    unsigned cls_n = 0;  // children classified for a query that ends or leaves
+    if (accept) {
+      if (first) {
+        // the level's first non-disjoint box ends the query (:243-252); the
+        // reference has checked the boxes up to it
+        cls_n = (unsigned)(Cb + nall - 1);
+        Cb += (int)si_[(kIntPf + par) * kLaneNT] + 1;
+        lane_write(a, col, hd && col[kColDrT0 * kLaneNT] < t0 ? kColDr : kColFr, Cb);
+        outcome = 1;
+      } else if (!hd || t0 < col[kColDrT0 * kLaneNT]) {
+        // an accepted box after the level's first: the drop record (:253-258)
+        lane_record(col, kColDr, pk, fabs(w), meta);
+        col[kColDrT0 * kLaneNT] = t0;
+        hd = true;
+      }
     }
-    // an accepted box after the level's first: the drop record (:253-258)
-    const bool drop = accept && !budget && col_lvl && (!hd || b.t0 < dr_t0);
-    if (drop) lane_record(col, kColDr, pk, wb, meta);
-    dr_t0 = drop ? b.t0 : dr_t0;
-    hd = hd || drop;
-    // refine along the level's split dimension: insert the child bit; the
-    // children are stored in push order.  Vertex-face: the upper child of a
-    // u / v split only inside u + v <= 1 (_kernel.py:276-310); t-split
-    // children are never clipped.
-    const bool refine = !disj && !budget && !accept;
-    const bool evict = refine && nn + 2 > kLaneArr;  // (never: levels <= kLaneCap)
-    const bool push = refine && !evict;
-    const int pos = sd == 0 ? suv : (sd == 1 ? nv : 0);
+    // refine along the level's split dimension: insert the child bit.
+    // Vertex-face: the upper child of a u / v split only inside u + v <= 1
+    // (_kernel.py:276-310); t-split children are never clipped.
+    const bool refine = !accept;
+    const int pos = (sd == 0 ? suv : 0) + (sd == 1 ? nv : 0);  // (selects, not a jump table)
     const unsigned long long lo = ((pk >> pos) << (pos + 1)) | (pk & ((1ull << pos) - 1ull));
     const unsigned long long hi = lo | (1ull << pos);
+    Box ba, bb;
+    ba.t0 = t0; ba.t1 = t0 + wt; ba.u0 = u0; ba.u1 = u0 + wu; ba.v0 = v0; ba.v1 = v0 + wv;
+    bb = ba;
+    {
+      // (midpoints of dyadic bounds: lo + w / 2 = 0.5 (lo + hi), exactly)
+      const double mt = t0 + lane_pow2(xt - nt - 1), mu = u0 + lane_pow2(1022 - nu),
+                   mv = v0 + lane_pow2(1022 - nv);
+      ba.t1 = sd == 0 ? mt : ba.t1; bb.t0 = sd == 0 ? mt : bb.t0;
+      ba.u1 = sd == 1 ? mu : ba.u1; bb.u0 = sd == 1 ? mu : bb.u0;
+      ba.v1 = sd == 2 ? mv : ba.v1; bb.v0 = sd == 2 ? mv : bb.v0;
+    }
     bool push_hi = true;
-    if (kind == 0) {
-      const bool hu = 0.5 * (b.u0 + b.u1) + b.v0 <= 1.0;
-      const bool hv = b.u0 + 0.5 * (b.v0 + b.v1) <= 1.0;
-      push_hi = sd == 0 ? true : (sd == 1 ? hu : hv);
+    if (kind == 0) push_hi = sd == 0 || bb.u0 + bb.v0 <= 1.0;  // (mid + the other lower bound)
+    double wa_, wb_;
+    int ca, cbx;
+    {
+      const double sep = col[kColSep * kLaneNT];
+      if (kind == 0) classify_pair<0>(P, ba, bb, eps, sep, ca, wa_, cbx, wb_);
+      else classify_pair<1>(P, ba, bb, eps, sep, ca, wa_, cbx, wb_);
     }
-    if (push) {
-      nxt[nn] = lo;
-      if (push_hi) nxt[nn + 1] = hi;
+    const bool na = refine && ca != kDisjoint;
+    const bool nb = refine && push_hi && cbx != kDisjoint;
+    {
+      // children: the lower one at the bottom, the upper one of a t split at
+      // the top, of a u / v split next at the bottom
+      const double ea = ca == kContained ? -wa_ : wa_;
+      const double eb = cbx == kContained ? -wb_ : wb_;
+      const int nA = (int)(nAB & 0xffffu), nB = (int)(nAB >> 16);
+      const int posb = sd == 0 ? kLaneArr - 1 - nB : nA + (na ? 1 : 0);
+      if (na) nxt[nA] = LaneEnt{lo, ea};
+      if (nb) nxt[posb] = LaneEnt{hi, eb};
+      const unsigned add = (na ? 1u : 0u) + (nb ? (sd == 0 ? 0x10000u : 1u) : 0u);
+      // the first segment's first bottom entry: its rank among all children
+      // in visiting order (t split: the run's lower children come first, one
+      // per parent; else push order); its first top entry: the children
+      // before its run plus its parent's index in the run
+      // (one slot each: a top entry's values stand until a bottom entry
+      // comes); with it the entry itself, the next level's first
+      if (nsn == 0 && (runAB & 0xffffu) == 0) {
+        const bool f_a = (add & 0xffffu) != 0;
+        const bool f_b = !f_a && (runAB >> 16) == 0 && (add >> 16) != 0;
+        if (f_a)
+          si_[kIntRk * kLaneNT] = (unsigned)(na ? (sd == 0 ? run_base + run_m : nall_next) : nall_next + 1);
+        if (f_b) si_[kIntRk * kLaneNT] = (unsigned)(run_base + run_m);
+        if (f_a || f_b) {
+          col[kColF0 * kLaneNT] = __longlong_as_double((long long)(f_a && na ? lo : hi));
+          col[(kColF0 + 1) * kLaneNT] = f_a && na ? ea : eb;
+        }
+      }
+      runAB += add;
+      nAB += add;
+      run_m += refine && sd == 0 ? 1 : 0;
+      nall_next += refine ? (push_hi ? 2 : 1) : 0;
     }
-    nxt0 = push && nn == 0 ? lo : nxt0;
-    nn += push ? (push_hi ? 2 : 1) : 0;
-    run_m += push && sd == 0 ? 1 : 0;
-    col_lvl = col_lvl || !disj;
-    outcome = evict ? 2 : outcome;
-    // advance to the next box
+    // advance to the next entry
     const bool go = outcome == 0;
     k += go ? 1 : 0;
-    seg_start = go ? n_start : seg_start;
-    seg_m = go ? n_m : seg_m;
-    seg_k = go ? n_k : seg_k;
-    seg_i = go ? n_i : seg_i;
-    if (go && n_newseg && seg_i + 1 < nseg) seg_mn = (int)segs[sgb + seg_i + 1];
-    pk = go ? pk_next : pk;
+    pk = go ? nx.x : pk;
+    w = go ? __longlong_as_double((long long)nx.y) : w;
     // ---- level end
     const bool lvl_end = go && k == ncur;
-    const bool close_last = lvl_end && run_m > 0;
-    if (close_last) snx[nsn] = (unsigned)run_m;
-    seg0 = close_last && nsn == 0 ? run_m : seg0;
-    nsn += close_last ? 1 : 0;
-    run_m = lvl_end ? 0 : run_m;
-    if (lvl_end && nn == 0) {
-      // queue exhausted (_kernel.py:321-324)
-      if (hd) {
-        lane_write(a, col, kColDr, C, 0);
+    close_segment(lvl_end && runAB != 0);
+    const int nnext = (int)((nAB & 0xffffu) + (nAB >> 16));
+    if (lvl_end && nnext == 0) {
+      const long long m = __double_as_longlong(col[kColMc * kLaneNT]);
+      if (Cb + nall + nall_next >= m) {
+        // (a budget return among the last level's disjoint boxes,
+        // _kernel.py:188-199: the light tier replays it)
+        outcome = 2;
       } else {
-        const Box z = {0, 0, 0, 0, 0, 0};
-        lane_emit(a, __double_as_longlong(col[kColQ * kLaneNT]), kFree, z, 0.0, C, 0, 0);
+        // queue exhausted (_kernel.py:321-324): every child was disjoint
+        // (and counted)
+        Cb += nall + nall_next;
+        cls_n = (unsigned)(Cb - 1);
+        if (hd) {
+          lane_write(a, col, kColDr, Cb);
+        } else {
+          const Box z = {0, 0, 0, 0, 0, 0};
+          write_result(a, __double_as_longlong(col[kColQ * kLaneNT]), kFree, z, 0.0, Cb, 0, 0);
+        }
+        outcome = 1;
       }
-      outcome = 1;
     }
-    const bool nl = lvl_end && nn > 0;  // the next level becomes current
-    cb = nl ? cb ^ kLaneArr : cb;
-    sgb = nl ? sgb ^ kLaneSeg : sgb;
-    const bool nilv = sd == 0;
-    if (nl && nilv && nsn > 1) seg_mn = (int)segs[sgb + 1];
-    ilv = nl ? nilv : ilv;
-    nseg = nl ? nsn : nseg;
-    seg_start = nl ? 0 : seg_start;
-    seg_k = nl ? 0 : seg_k;
-    seg_i = nl ? 0 : seg_i;
-    seg_m = nl ? seg0 : seg_m;
-    ncur = nl ? nn : ncur;
-    k = nl ? 0 : k;
-    pk = nl ? nxt0 : pk;
-    nn = nl ? 0 : nn;
-    nsn = nl ? 0 : nsn;
-    run = nl ? ~0ull : run;
-    L += nl ? 1 : 0;
-    col_lvl = nl ? false : col_lvl;
-    // every refining box of the level split along sd
-    const bool st_ = nl && sd == 0, su_ = nl && sd == 1, sv_ = nl && sd == 2;
-    nt += st_ ? 1 : 0; wt = st_ ? 0.5 * wt : wt;
-    nu += su_ ? 1 : 0; wu = su_ ? 0.5 * wu : wu;
-    nv += sv_ ? 1 : 0; wv = sv_ ? 0.5 * wv : wv;
-    const int ns = sd == 0 ? nt : (sd == 1 ? nu : nv);
-    // a level too large for this tier (or a lattice about to leave its index
-    // range) is handed over to the light tier; so is, once this kind's queue
-    // is empty, the level of a query that has already run a while: the
-    // lane tier's tail (lanes idle while the last queries finish one box at
-    // a time) becomes level-parallel work for the light tier
-    outcome = nl && (ncur > kLaneCap || ns > kLaneMaxSplits || L > kLaneMaxLevel ||
-                     (dry && C >= kLaneTailChecks))
-                  ? 3 : outcome;
-    sd = nl ? lane_split_dim(wt, wu, wv, kap) : sd;
+    const bool nl = lvl_end && nnext > 0;  // the next level becomes current
+    if (nl) {
+      cb ^= kLaneArr;
+      Cb += nall;
+      nall = nall_next;
+      ncur = nnext;
+      k = 0;
+      // the level's first entry (the first segment's bottom part, else its
+      // top part); the visiting state is the one after it
+      const bool fa = (seg0 & 0xffffu) != 0;
+      pk = (unsigned long long)__double_as_longlong(col[kColF0 * kLaneNT]);
+      w = col[(kColF0 + 1) * kLaneNT];
+      rAB = seg0 - (fa ? 1u : 0x10000u);
+      pa = fa ? 1 : 0;
+      si = 0;
+      nseg = nsn;
+      sn = seg1;
+      nAB = runAB = 0u;
+      nsn = run_m = run_base = nall_next = 0;
+      run = ~0ull;
+      // every refining box of the level split along sd
+      nt += sd == 0 ? 1 : 0;
+      nu += sd == 1 ? 1 : 0;
+      nv += sd == 2 ? 1 : 0;
+      const int ns = sd == 0 ? nt : (sd == 1 ? nu : nv);
+      // a lattice about to leave its index range, or a level that could
+      // reach the budget: the query restarts in the light tier.  A level too
+      // large for this tier is handed over to the light tier; so is, once
+      // this kind's queue is empty, the level of a query that has already
+      // run a while: the lane tier's tail (lanes idle while the last queries
+      // finish one box at a time) becomes level-parallel work for the light
+      // tier.  (Not a level whose first box ends the query: the lane
+      // finishes that one itself.)
+      const long long m = __double_as_longlong(col[kColMc * kLaneNT]);
+      if (ns > kLaneMaxSplits || nt + nu + nv > kLaneMaxLevel || Cb + nall >= m) {
+        outcome = 2;
+      } else if (ncur > kLaneCap || (dry && Cb + nall >= kLaneTailChecks)) {
+        const bool acc0 = fabs(w) < col[kColDelta * kLaneNT] || __double_as_longlong(w) < 0;
+        outcome = acc0 ? outcome : 3;
+      }
+      sd = lane_split_dim(lane_pow2(xt - nt), lane_pow2(1023 - nu), lane_pow2(1023 - nv), kap);
+    }
     if (outcome == 1) {
-      st.checks += (unsigned)(C - 1);  // checks of finished queries (root: prologue's)
-      st.done += 1;
+      si_[kIntChecks * kLaneNT] += (unsigned)(Cb - 1);  // checks of finished queries (root: prologue's)
+      si_[kIntCls * kLaneNT] += cls_n;
+      si_[kIntDone * kLaneNT] += 1u;
       state = 0;
     } else if (outcome >= 2) {
       // to the light tier: with the current level handed over (outcome 3,
       // room permitting), else restarting from the root
       unsigned int hidx = 0xffffffffu;
+      // checks the reference has spent when it starts on the handed-over
+      // boxes' level, plus that level's disjoint boxes
+      const int Ch = Cb + nall - ncur;
       if (outcome == 3) {
         const unsigned long long h = atomicAdd(io.hand_count, 1ull);
         const unsigned long long off = atomicAdd(io.pool_count, (unsigned long long)ncur);
         if ((long long)h < io.hand_cap && (long long)(off + ncur) <= io.pool_cap) {
           hidx = (unsigned int)h;
-          const unsigned long long* cw = lb + cb;
-          int ss = 0, sm = seg_m, sk = 0, si = 0;
+          const LaneEnt* cw = ent + cb;
+          const double t_max = col[kColTmax * kLaneNT];
           double prev = -1.0;
-          for (int j = 0; j < ncur; ++j) {
-            int pos = j;
-            if (ilv) {
-              if (sk == 2 * sm) { ss += 2 * sm; ++si; sm = (int)segs[sgb + si]; sk = 0; }
-              pos = sk < sm ? ss + 2 * sk : ss + 2 * (sk - sm) + 1;
-              ++sk;
+          int qa = 0, qb = kLaneArr - 1, j = 0;
+          for (int s = 0; s < nseg; ++s) {
+            const unsigned sg = s == 0 ? seg0 : segs[cb + s];
+            const int ca_ = (int)(sg & 0xffffu), cb_ = (int)(sg >> 16);
+            for (int i = 0; i < ca_ + cb_; ++i, ++j) {
+              const int p = i < ca_ ? qa++ : qb--;
+              const Box bx = lane_box(cw[p].pk, nt, nu, nv, t_max);
+              io.pbox[off + j] = bx;
+              io.pflag[off + j] = (uint8_t)(j == 0 || bx.t0 != prev ? 128 : 0);  // the engine's kHead
+              prev = bx.t0;
             }
-            const Box bb = lane_box(cw[pos], nt, nu, nv, col[kColTmax * kLaneNT]);
-            io.pbox[off + j] = bb;
-            io.pflag[off + j] = (uint8_t)(j == 0 || bb.t0 != prev ? 128 : 0);  // the engine's kHead
-            prev = bb.t0;
           }
           Hand& H = io.hand[h];
-          H.C = C;
+          H.C = Ch;
           H.off = (long long)off;
-          H.level = L;
+          H.level = nt + nu + nv;
           H.n = ncur;
-          const double t_max = col[kColTmax * kLaneNT];
           H.rec[0].b = lane_record_box(col, kColFr, t_max);
           H.rec[0].codom = col[(kColFr + 1) * kLaneNT];
           H.rec[0].level = lane_record_level(col, kColFr);
           H.rec[1].b = lane_record_box(col, kColDr, t_max);
           H.rec[1].codom = col[(kColDr + 1) * kLaneNT];
           H.rec[1].level = lane_record_level(col, kColDr);
-          H.have_first = hf ? 1 : 0;
+          H.have_first = 1;
           H.have_drop = hd ? 1 : 0;
-          st.handed += 1;
+          si_[kIntHanded * kLaneNT] += 1u;
         }
       }
       const unsigned long long e = atomicAdd(io.out_count, 1ull);
       io.out[e] = Pre{__double_as_longlong(col[kColQ * kLaneNT]), 0.0, 0u, hidx};
-      st.evicted += 1;
+      si_[kIntEvicted * kLaneNT] += 1u;
+      si_[kIntCls * kLaneNT] += (unsigned)(Cb + nall + nall_next - 1);
       // (a restart repeats the lane's checks in the light tier)
-      if (hidx == 0xffffffffu) st.wasted += (unsigned)(C - 1);
-      else st.checks += (unsigned)(C - 1);  // (on the reference's path: the light tier goes on)
+      if (hidx == 0xffffffffu) si_[kIntWasted * kLaneNT] += (unsigned)(Cb + nall - 1);
+      else si_[kIntChecks * kLaneNT] += (unsigned)(Ch - 1);  // (on the reference's path: the light tier goes on)
       state = 0;
     }
   }
-  lane_flush(io, st, kind);
+  lane_flush(io, si_, kind);
 }
 
+// dynamic shared memory of one lane CTA: the columns, the 32-bit slots, the
+// warps' claim words
+constexpr size_t kLaneSmemBytes =
+    (size_t)kLaneCol * kLaneNT * 8 + (size_t)kLaneInt * kLaneNT * 4 + 4 * (kLaneNT / 32) * 4;
+
 __global__ void __launch_bounds__(kLaneNT, TCCD_NMINB) lane_kernel(Args a, LaneIO io) {
-  __shared__ double Ps[kLaneCol * kLaneNT];
+  extern __shared__ __align__(16) unsigned char lane_smem[];
+  double* const Ps = reinterpret_cast<double*>(lane_smem);
+  unsigned* const Si = reinterpret_cast<unsigned*>(Ps + kLaneCol * kLaneNT);
+  unsigned* const Sw = Si + kLaneInt * kLaneNT;
   const long long gt = (long long)blockIdx.x * kLaneNT + threadIdx.x;
   unsigned long long* lb = io.scratch + gt * kLaneScratchWords;
   double* col = Ps + threadIdx.x;
+  unsigned* si = Si + threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < kLaneInt; ++i) si[i * kLaneNT] = 0u;
   const unsigned long long nvf = io.count[0], nee = io.count[1];
   // first kind of this warp: warps split between the kinds in proportion to
   // their queues; a warp whose queue runs dry moves to the other one
   const long long gw = gt >> 5, nw = (long long)gridDim.x * (kLaneNT / 32);
   int kind = (nvf + nee) > 0 && (unsigned long long)gw * (nvf + nee) < nee * (unsigned long long)nw;
-  for (int pass = 0; pass < 2; ++pass, kind ^= 1) lane_loop(a, io, col, lb, kind);
+  for (int pass = 0; pass < 2; ++pass, kind ^= 1)
+    lane_loop(a, io, col, si, Sw + 4 * (threadIdx.x >> 5), lb, kind);
 }
 
 }  // namespace tccd
