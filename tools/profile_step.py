@@ -33,19 +33,18 @@ if args.config == 2:
 from paper_2009_13349_b200 import _lib, solver  # noqa: E402
 for r in range(args.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(solver.STAGES))]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(64)]
+    info = {}
     e0.record()
     out = solve_batch(pts, kind, outputs=("status", "toi", "checks"), device=dev,
                       separation=w.separation, heavy_only=args.heavy_only, stats=True,
                       heavy_blocks=args.heavy_blocks, lanes=not args.no_lanes,
-                      events=ev if args.queries <= solver.CHUNK else None, **kw)
+                      events=ev, info=info, **kw)
     e1.record()
     torch.cuda.synchronize()
     st = out["stats"].tolist()
-    stages = ""
-    if args.queries <= solver.CHUNK:
-        t = [e0.elapsed_time(ev[0])] + [ev[j].elapsed_time(ev[j + 1]) for j in range(len(ev) - 1)]
-        stages = " stages " + "/".join(f"{nm} {x:.2f}" for nm, x in zip(solver.STAGES, t))
+    t = solver.stage_times(e0, ev, info["event_stages"])
+    stages = " stages " + "/".join(f"{nm} {x:.2f}" for nm, x in t.items())
     print(f"rep {r}: {e0.elapsed_time(e1):.2f} ms{stages}  checks {int(out['checks'].sum())} "
           f"lane q {st[_lib.STAT_LANE_QUERIES]} evicted {st[_lib.STAT_LANE_EVICTED]} "
           f"giant {st[_lib.STAT_GIANT_QUERIES]} medium {st[_lib.STAT_MEDIUM_QUERIES]} "
