@@ -296,64 +296,6 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   bool n_pend = false, n_have = false;
   unsigned claim_ret = 0;  // (lane 0's register)
   for (;;) {
-    // ---- new queries, copied by the whole warp.  A lane that took a queue
-    // entry last iteration has its 64-byte record in its column now: the
-    // warp copies that query's 24 coordinates and 4 parameters there (one
-    // cp.async per lane, coalesced); a lane whose coordinates were copied
-    // last iteration starts on its query.  (A lane copying for itself spent
-    // ~100 instructions with one or two lanes active, nearly every
-    // iteration: some lane of a warp starts a query about once an
-    // iteration.)
-    {
-      const unsigned m1 = __ballot_sync(FULL, state == 1);
-      const unsigned m2 = __ballot_sync(FULL, state == 2);
-      if (m1 | m2) {
-        // every lane's copies on behalf of the others have landed
-        cp_async_wait_all();
-        __syncwarp();
-      }
-      for (unsigned m = m1; m; m &= m - 1) {
-        const int t = __ffs((int)m) - 1;
-        double* const tc = col + (t - lane);  // the target lane's column
-        const long long qn = __double_as_longlong(tc[kColQ * kLaneNT]);
-        if (lane < 24) {
-          cp_async8(tc + lane * kLaneNT, a.points + 24 * qn + lane);
-        } else if (lane < 28) {
-          // lanes 24..27: separation, delta, t_max, m_I (per query, else the call's)
-          const int j = lane - 24;
-          const double* src = j == 0 ? a.sep : (j == 1 ? a.delta : (j == 2 ? a.t_max
-                                     : reinterpret_cast<const double*>(a.max_checks)));
-          const double all = j == 0 ? a.sep_all : (j == 1 ? a.delta_all : (j == 2 ? a.t_max_all
-                                     : __longlong_as_double(a.max_checks_all)));
-          double* const dst = tc + (kColSep + j) * kLaneNT;
-          if (src) cp_async8(dst, src + qn);
-          else *dst = all;
-        }
-      }
-    }
-    if (state == 2) {
-      // level 0: the root, classified by the prologue (non-disjoint, to be
-      // refined: one check, rank 0); this lane's first iteration records it
-      // as the level's first box and classifies its two children
-      Cb = 0; nall = 1;
-      si_[kIntPf * kLaneNT] = 0u;
-      nt = nu = nv = 0;
-      // (t_max is a power of two in the normal range: the prologue's test)
-      xt = (int)(__double2hiint(col[kColTmax * kLaneNT]) >> 20);
-      sd = lane_split_dim(lane_pow2(xt), 1.0, 1.0, kap);
-      cb = 0;
-      ncur = 1; k = 0;
-      rAB = 0; pa = 0; si = 0; nseg = 1; sn = 0;
-      pk = 0; w = col[kColWb * kLaneNT];
-      nAB = runAB = 0;
-      nsn = run_m = run_base = nall_next = 0;
-      run = ~0ull;
-      hd = false;
-      state = 3;
-    } else if (state == 1) {
-      state = 2;
-    }
-    // ---- queue claims
     if (n_pend) {
       const unsigned base = __shfl_sync(FULL, claim_ret, 0);
       const unsigned total = wq[3];
@@ -378,20 +320,17 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     }
     const unsigned need = __ballot_sync(FULL, state == 0);
     if (need && r_left > 0) {
-      // the first idle lanes take the range's next entries; lanes 0..7 copy
-      // each one's record into the taker's column
+      const int rank = __popc(need & ((1u << lane) - 1u));
       const int take = __popc(need) < r_left ? __popc(need) : r_left;
       const unsigned r_base = wq[0];
-      unsigned m = need;
-      for (int i = 0; i < take; ++i, m &= m - 1) {
-        const int t = __ffs((int)m) - 1;
-        if (lane < 8) {
-          const unsigned kq = r_base + (unsigned)i;
-          const double* src = reinterpret_cast<const double*>(
-              &io.rec[kind ? io.rec_cap - 1 - (long long)kq : (long long)kq]);
-          cp_async8(col + (t - lane) + (kColQ + lane) * kLaneNT, src + lane);
-        }
-        if (lane == t) state = 1;
+      if (state == 0 && rank < take) {
+        // start the copy of the entry's record
+        const unsigned kq = r_base + rank;
+        const double* src = reinterpret_cast<const double*>(
+            &io.rec[kind ? io.rec_cap - 1 - (long long)kq : (long long)kq]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cp_async8(col + (kColQ + i) * kLaneNT, src + i);
+        state = 1;
       }
       __syncwarp();
       wq[0] = r_base + take;
@@ -401,6 +340,47 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       // nothing in flight: done once the queue is known empty
       if (dry && r_left == 0 && !n_have && !n_pend) break;
       continue;
+    }
+    if (state == 0) continue;
+    if (state == 1) {
+      // the record has landed (one iteration later): copy the coordinates
+      // and the per-query parameters
+      cp_async_wait_all();
+      const long long qn = __double_as_longlong(col[kColQ * kLaneNT]);
+      const double* src = a.points + 24 * qn;
+#pragma unroll
+      for (int i = 0; i < 24; ++i) cp_async8(col + i * kLaneNT, src + i);
+      if (a.sep) cp_async8(col + kColSep * kLaneNT, a.sep + qn);
+      else col[kColSep * kLaneNT] = a.sep_all;
+      if (a.delta) cp_async8(col + kColDelta * kLaneNT, a.delta + qn);
+      else col[kColDelta * kLaneNT] = a.delta_all;
+      if (a.t_max) cp_async8(col + kColTmax * kLaneNT, a.t_max + qn);
+      else col[kColTmax * kLaneNT] = a.t_max_all;
+      if (a.max_checks) cp_async8(col + kColMc * kLaneNT, reinterpret_cast<const double*>(a.max_checks + qn));
+      else col[kColMc * kLaneNT] = __longlong_as_double(a.max_checks_all);
+      state = 2;
+      continue;
+    }
+    if (state == 2) {
+      cp_async_wait_all();
+      // level 0: the root, classified by the prologue (non-disjoint, to be
+      // refined: one check, rank 0); this lane's first iteration records it
+      // as the level's first box and classifies its two children
+      Cb = 0; nall = 1;
+      si_[kIntPf * kLaneNT] = 0u;
+      nt = nu = nv = 0;
+      // (t_max is a power of two in the normal range: the prologue's test)
+      xt = (int)(__double2hiint(col[kColTmax * kLaneNT]) >> 20);
+      sd = lane_split_dim(lane_pow2(xt), 1.0, 1.0, kap);
+      cb = 0;
+      ncur = 1; k = 0;
+      rAB = 0; pa = 0; si = 0; nseg = 1; sn = 0;
+      pk = 0; w = col[kColWb * kLaneNT];
+      nAB = runAB = 0;
+      nsn = run_m = run_base = nall_next = 0;
+      run = ~0ull;
+      hd = false;
+      state = 3;
     }
     if (state != 3) continue;  // (idle: this kind's queue ran dry)
 
