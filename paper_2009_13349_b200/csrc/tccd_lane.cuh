@@ -50,10 +50,11 @@
 // top part: no entry is ever moved.
 //
 // Latency: the entry of the next box is loaded while the current box's
-// children are classified; a lane that takes a new query copies its 64-byte
-// record (index, filters, kappas) and then the query's coordinates and
-// parameters into its shared-memory column with cp.async, one iteration
-// apart, and starts on it the iteration after, so neither stalls the warp.
+// children are classified; with each claimed range of queue entries the warp
+// fetches the entries' query indices, so a lane that takes a new query
+// copies its 64-byte record (index, filters, kappas), the query's
+// coordinates and its parameters into its shared-memory column with
+// cp.async in one go and starts on it the iteration after.
 //
 // A query leaves this tier when its next level has more than kLaneCap
 // non-disjoint boxes (the level arrays hold 2 kLaneCap entries, so the
@@ -88,6 +89,10 @@ constexpr int kLaneMaxLevel = 62;   // ti | ui | vi fits one 64-bit word
 #define TCCD_LANE_TAIL 128
 #endif
 constexpr int kLaneTailChecks = TCCD_LANE_TAIL;  // (tail handover threshold)
+#ifndef TCCD_LANE_TAIL_WIDTH
+#define TCCD_LANE_TAIL_WIDTH 16
+#endif
+constexpr int kLaneTailWidth = TCCD_LANE_TAIL_WIDTH;  // smallest level handed over in the tail
 #ifndef TCCD_LANE_CLAIM
 #define TCCD_LANE_CLAIM 32
 #endif
@@ -242,8 +247,8 @@ __device__ __forceinline__ double lane_pow2(int x) { return __hiloint2double(x <
 // One kind's queue (kind is warp-uniform; only the classification is
 // specialized on it, so the loop's code exists once).
 __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, double* col,
-                                          unsigned* si_, unsigned* wq, unsigned long long* lb,
-                                          const int kind) {
+                                          unsigned* si_, unsigned* wq, long long* sq,
+                                          unsigned long long* lb, const int kind) {
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const ColP<kLaneNT> P{col};
@@ -252,7 +257,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   LaneEnt* const ent = reinterpret_cast<LaneEnt*>(lb);  // [2][kLaneArr]
   unsigned int* const segs = reinterpret_cast<unsigned int*>(lb + 2 * kLaneArr * 2);  // [2][kLaneSeg]
   bool dry = false;  // (warp-uniform) this kind's queue is empty
-  int state = 0;     // 0 idle, 1 record in flight, 2 coordinates in flight, 3 active
+  int state = 0;     // 0 idle, 2 record and coordinates in flight, 3 active
   // checks before the current level; the level's boxes (all of them, the
   // checks the reference spends on it).  (A lane query stays far below 2^31
   // checks: <= 62 levels of <= 4 kLaneCap boxes.)  The visiting rank, among
@@ -290,9 +295,14 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   // the atomic's result is read an iteration later, so its latency is spent
   // classifying.  (All of this is warp-uniform; the ranges live in the
   // warp's shared-memory words wq: [0] current base, [1] next base, [2] next
-  // length, [3] the queue's length.)
+  // length, [3] the queue's length.)  With a range's base the warp fetches
+  // the query indices of its entries (one cp.async per lane into sq, double
+  // buffered), so a lane that takes an entry knows its query at once and
+  // copies record, coordinates and parameters together.
+  static_assert(kLaneClaim == 32, "one entry of a claimed range per lane; ranges start at multiples of 32");
   wq[3] = (unsigned)io.count[kind];  // (a chunk's queue: <= 2^26 entries)
   int r_left = 0;
+  int qb = 0;  // sq buffer of the current range
   bool n_pend = false, n_have = false;
   unsigned claim_ret = 0;  // (lane 0's register)
   for (;;) {
@@ -303,14 +313,25 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       if (base >= total) {
         dry = true;
       } else {
+        const unsigned nl_ = total - base < (unsigned)kLaneClaim ? total - base : (unsigned)kLaneClaim;
         wq[1] = base;
-        wq[2] = total - base < (unsigned)kLaneClaim ? total - base : (unsigned)kLaneClaim;
+        wq[2] = nl_;
         n_have = true;
+        if ((unsigned)lane < nl_) {
+          const long long kq = (long long)base + lane;
+          cp_async8(reinterpret_cast<double*>(sq + (qb ^ 1) * kLaneClaim + lane),
+                    reinterpret_cast<const double*>(&io.rec[kind ? io.rec_cap - 1 - kq : kq]));
+        }
       }
     }
     if (r_left == 0 && n_have) {
+      // (the range's query indices have landed: fetched an atomic's round
+      // trip and at least one iteration ago)
+      cp_async_wait_all();
+      __syncwarp();
       wq[0] = wq[1];
       r_left = (int)wq[2];
+      qb ^= 1;
       n_have = false;
     }
     if (!dry && !n_pend && !n_have && r_left < kLaneClaim / 2) {
@@ -324,13 +345,26 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       const int take = __popc(need) < r_left ? __popc(need) : r_left;
       const unsigned r_base = wq[0];
       if (state == 0 && rank < take) {
-        // start the copy of the entry's record
+        // start the copies of the entry's record, its query's coordinates
+        // and the per-query parameters
         const unsigned kq = r_base + rank;
         const double* src = reinterpret_cast<const double*>(
             &io.rec[kind ? io.rec_cap - 1 - (long long)kq : (long long)kq]);
 #pragma unroll
         for (int i = 0; i < 8; ++i) cp_async8(col + (kColQ + i) * kLaneNT, src + i);
-        state = 1;
+        const long long qn = sq[qb * kLaneClaim + (kq & (kLaneClaim - 1))];
+        const double* pts = a.points + 24 * qn;
+#pragma unroll
+        for (int i = 0; i < 24; ++i) cp_async8(col + i * kLaneNT, pts + i);
+        if (a.sep) cp_async8(col + kColSep * kLaneNT, a.sep + qn);
+        else col[kColSep * kLaneNT] = a.sep_all;
+        if (a.delta) cp_async8(col + kColDelta * kLaneNT, a.delta + qn);
+        else col[kColDelta * kLaneNT] = a.delta_all;
+        if (a.t_max) cp_async8(col + kColTmax * kLaneNT, a.t_max + qn);
+        else col[kColTmax * kLaneNT] = a.t_max_all;
+        if (a.max_checks) cp_async8(col + kColMc * kLaneNT, reinterpret_cast<const double*>(a.max_checks + qn));
+        else col[kColMc * kLaneNT] = __longlong_as_double(a.max_checks_all);
+        state = 2;
       }
       __syncwarp();
       wq[0] = r_base + take;
@@ -342,25 +376,6 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       continue;
     }
     if (state == 0) continue;
-    if (state == 1) {
-      // the record has landed (one iteration later): copy the coordinates
-      // and the per-query parameters
-      cp_async_wait_all();
-      const long long qn = __double_as_longlong(col[kColQ * kLaneNT]);
-      const double* src = a.points + 24 * qn;
-#pragma unroll
-      for (int i = 0; i < 24; ++i) cp_async8(col + i * kLaneNT, src + i);
-      if (a.sep) cp_async8(col + kColSep * kLaneNT, a.sep + qn);
-      else col[kColSep * kLaneNT] = a.sep_all;
-      if (a.delta) cp_async8(col + kColDelta * kLaneNT, a.delta + qn);
-      else col[kColDelta * kLaneNT] = a.delta_all;
-      if (a.t_max) cp_async8(col + kColTmax * kLaneNT, a.t_max + qn);
-      else col[kColTmax * kLaneNT] = a.t_max_all;
-      if (a.max_checks) cp_async8(col + kColMc * kLaneNT, reinterpret_cast<const double*>(a.max_checks + qn));
-      else col[kColMc * kLaneNT] = __longlong_as_double(a.max_checks_all);
-      state = 2;
-      continue;
-    }
     if (state == 2) {
       cp_async_wait_all();
       // level 0: the root, classified by the prologue (non-disjoint, to be
@@ -578,15 +593,15 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       // a lattice about to leave its index range, or a level that could
       // reach the budget: the query restarts in the light tier.  A level too
       // large for this tier is handed over to the light tier; so is, once
-      // this kind's queue is empty, the level of a query that has already
-      // run a while: the lane tier's tail (lanes idle while the last queries
-      // finish one box at a time) becomes level-parallel work for the light
-      // tier.  (Not a level whose first box ends the query: the lane
+      // this kind's queue is empty, a level of kLaneTailWidth boxes or more
+      // of a query that has already run a while: the lane tier's tail (lanes
+      // idle while the last wide queries finish one box at a time) becomes
+      // level-parallel work for the light tier; narrow levels finish here.  (Not a level whose first box ends the query: the lane
       // finishes that one itself.)
       const long long m = __double_as_longlong(col[kColMc * kLaneNT]);
       if (ns > kLaneMaxSplits || nt + nu + nv > kLaneMaxLevel || Cb + nall >= m) {
         outcome = 2;
-      } else if (ncur > kLaneCap || (dry && Cb + nall >= kLaneTailChecks)) {
+      } else if (ncur > kLaneCap || (dry && Cb + nall >= kLaneTailChecks && ncur >= kLaneTailWidth)) {
         const bool acc0 = fabs(w) < col[kColDelta * kLaneNT] || __double_as_longlong(w) < 0;
         outcome = acc0 ? outcome : 3;
       }
@@ -655,13 +670,14 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
 
 // dynamic shared memory of one lane CTA: the columns, the 32-bit slots, the
 // warps' claim words
-constexpr size_t kLaneSmemBytes =
-    (size_t)kLaneCol * kLaneNT * 8 + (size_t)kLaneInt * kLaneNT * 4 + 4 * (kLaneNT / 32) * 4;
+constexpr size_t kLaneSmemBytes = (size_t)kLaneCol * kLaneNT * 8 + (size_t)kLaneInt * kLaneNT * 4 +
+                                  (size_t)(kLaneNT / 32) * (2 * kLaneClaim * 8 + 4 * 4);
 
 __global__ void __launch_bounds__(kLaneNT, TCCD_NMINB) lane_kernel(Args a, LaneIO io) {
   extern __shared__ __align__(16) unsigned char lane_smem[];
   double* const Ps = reinterpret_cast<double*>(lane_smem);
-  unsigned* const Si = reinterpret_cast<unsigned*>(Ps + kLaneCol * kLaneNT);
+  long long* const Sq = reinterpret_cast<long long*>(Ps + kLaneCol * kLaneNT);
+  unsigned* const Si = reinterpret_cast<unsigned*>(Sq + (kLaneNT / 32) * 2 * kLaneClaim);
   unsigned* const Sw = Si + kLaneInt * kLaneNT;
   const long long gt = (long long)blockIdx.x * kLaneNT + threadIdx.x;
   unsigned long long* lb = io.scratch + gt * kLaneScratchWords;
@@ -675,7 +691,8 @@ __global__ void __launch_bounds__(kLaneNT, TCCD_NMINB) lane_kernel(Args a, LaneI
   const long long gw = gt >> 5, nw = (long long)gridDim.x * (kLaneNT / 32);
   int kind = (nvf + nee) > 0 && (unsigned long long)gw * (nvf + nee) < nee * (unsigned long long)nw;
   for (int pass = 0; pass < 2; ++pass, kind ^= 1)
-    lane_loop(a, io, col, si, Sw + 4 * (threadIdx.x >> 5), lb, kind);
+    lane_loop(a, io, col, si, Sw + 4 * (threadIdx.x >> 5),
+              Sq + (threadIdx.x >> 5) * 2 * kLaneClaim, lb, kind);
 }
 
 }  // namespace tccd
