@@ -90,7 +90,7 @@ constexpr int kLaneMaxLevel = 62;   // ti | ui | vi fits one 64-bit word
 #endif
 constexpr int kLaneTailChecks = TCCD_LANE_TAIL;  // (tail handover threshold)
 #ifndef TCCD_LANE_TAIL_WIDTH
-#define TCCD_LANE_TAIL_WIDTH 16
+#define TCCD_LANE_TAIL_WIDTH 0
 #endif
 constexpr int kLaneTailWidth = TCCD_LANE_TAIL_WIDTH;  // smallest level handed over in the tail
 #ifndef TCCD_LANE_CLAIM
@@ -593,10 +593,11 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       // a lattice about to leave its index range, or a level that could
       // reach the budget: the query restarts in the light tier.  A level too
       // large for this tier is handed over to the light tier; so is, once
-      // this kind's queue is empty, a level of kLaneTailWidth boxes or more
-      // of a query that has already run a while: the lane tier's tail (lanes
-      // idle while the last wide queries finish one box at a time) becomes
-      // level-parallel work for the light tier; narrow levels finish here.  (Not a level whose first box ends the query: the lane
+      // this kind's queue is empty, the level of a query that has already
+      // run a while: the lane tier's tail (lanes idle while the last queries
+      // finish one box at a time) becomes level-parallel work for the light
+      // tier.  (kLaneTailWidth > 0 keeps narrower levels here: 8 / 16 measured
+      // no gain on 5e7 config-3 queries and doubled config 0's 1.3 ms.)  (Not a level whose first box ends the query: the lane
       // finishes that one itself.)
       const long long m = __double_as_longlong(col[kColMc * kLaneNT]);
       if (ns > kLaneMaxSplits || nt + nu + nv > kLaneMaxLevel || Cb + nall >= m) {
