@@ -227,7 +227,10 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
 // ===========================================================================
 constexpr int kPrologueThreads = 128;
 
-__global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long long lo,
+#ifndef TCCD_PRO_MINB
+#define TCCD_PRO_MINB 4
+#endif
+__global__ void __launch_bounds__(kPrologueThreads, TCCD_PRO_MINB) prologue_kernel(Args a, long long lo,
                                                                     long long cnt, Pre* queue,
                                                                     unsigned long long* qcount,
                                                                     LaneRec* lq, long long lq_cap,
@@ -237,9 +240,19 @@ __global__ void __launch_bounds__(kPrologueThreads) prologue_kernel(Args a, long
   const int nb = (int)min((long long)kPrologueThreads, lo + cnt - base);
   // coalesced staging of the block's 24-double records
   {
+    // (cp.async: the tile's 12 x 16 bytes per thread are all in flight at
+    // once, without a round trip through registers)
     const double2* src = reinterpret_cast<const double2*>(a.points + 24 * base);
     double2* dst = reinterpret_cast<double2*>(tile);
+#ifdef TCCD_PRO_SYNC_LOAD
     for (int i = threadIdx.x; i < nb * 12; i += kPrologueThreads) dst[i] = src[i];
+#else
+    for (int i = threadIdx.x; i < nb * 12; i += kPrologueThreads) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + i);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + i) : "memory");
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+#endif
   }
   __syncthreads();
   const int t = threadIdx.x;
