@@ -59,9 +59,9 @@ def test_samples_vs_oracle_both_paths(cuda, config, start, count, sep, lanes):
 
 def test_lane_tier_takes_the_shallow_queries(cuda):
     """On simulation-shaped queries the lane tier finishes most survivors of
-    the root check; the rest (levels above 64 boxes, and the queries still
-    running when the queue runs dry: the lane tier's tail) go to the light
-    tier with their current level."""
+    the root check; the rest (levels above 128 non-disjoint boxes, and the
+    queries still running when the queue runs dry: the lane tier's tail) go to
+    the light tier with their current level."""
     from paper_2009_13349_b200 import _lib
     from paper_2009_13349_b200 import workloads as W
     w = W.generate(3, 300_000, 200_000)
@@ -75,6 +75,49 @@ def test_lane_tier_takes_the_shallow_queries(cuda):
     assert ev < 0.25 * entered  # (200k queries: the tail is a large share)
     # with room in the handover pool every eviction carries its level
     assert st[_lib.STAT_LANE_HANDED] == ev and st[_lib.STAT_LANE_WASTED] == 0
+
+
+@pytest.mark.parametrize("config,count", [(3, 60_000), (1, 12_000)])
+def test_lane_tier_small_budgets(cuda, config, count):
+    """Per-query budgets from 2 to a few thousand checks: the lane tier has no
+    budget events of its own -- a level whose boxes could reach m_I, or a last
+    level of disjoint boxes that could, sends the query to the light tier to
+    restart (pkg/src/ccdkit/_kernel.py:188-213) -- so budget returns at every
+    depth must come out as the reference's."""
+    from paper_2009_13349_b200 import _lib, solve_batch
+    from paper_2009_13349_b200 import workloads as W
+    w = W.generate(config, 40_000, count)
+    rng = np.random.default_rng(17)
+    mc = rng.choice(np.array([2, 3, 4, 5, 8, 13, 17, 33, 50, 64, 100, 129, 257, 700, 1500, 4000],
+                             dtype=np.int64), size=w.n)
+    ref = oracle.solve_batch(w.points, w.kind, w.delta, mc, w.separation, w.t_max)
+    got = solve_batch(torch.from_numpy(w.points), torch.from_numpy(w.kind), delta=w.delta,
+                      max_checks=torch.from_numpy(mc), separation=w.separation, device=cuda,
+                      raise_on_error=False, stats=True)
+    st = got.pop("stats").cpu().numpy()
+    assert_same_results(_np(got), ref, f"c{config} small budgets")
+    assert int(np.asarray(ref["early"]).sum()) > 0          # budget returns happen
+    assert st[_lib.STAT_LANE_WASTED] > 0                    # and some were lane restarts
+
+
+def test_lane_tier_dyadic_t_max_range(cuda):
+    """Per-query dyadic t_max from 1 down to subnormal powers of two: the lane
+    tier builds its box widths from t_max's exponent field and takes t_max >=
+    2^-900 (62 halvings stay normal); smaller ones go to the group tiers.
+    Both must match the reference's boxes bit for bit."""
+    from paper_2009_13349_b200 import _lib, solve_batch
+    from paper_2009_13349_b200 import workloads as W
+    w = W.generate(3, 900_000, 40_000)
+    exps = np.array([0, -1, -2, -7, -20, -52, -200, -899, -900, -901, -1000, -1022, -1023, -1070])
+    tm = np.ldexp(1.0, exps[np.arange(w.n) % len(exps)])
+    ref = oracle.solve_batch(w.points, w.kind, w.delta, w.max_checks, w.separation, tm)
+    got = solve_batch(torch.from_numpy(w.points), torch.from_numpy(w.kind), delta=w.delta,
+                      max_checks=w.max_checks, separation=w.separation, t_max=torch.from_numpy(tm),
+                      device=cuda, raise_on_error=False, stats=True)
+    st = got.pop("stats").cpu().numpy()
+    assert_same_results(_np(got), ref, "dyadic t_max range")
+    assert st[_lib.STAT_LANE_QUERIES] > 0
+    assert int((np.asarray(ref["status"]) == 1).sum()) > 0
 
 
 @pytest.mark.parametrize("config,count,kw", [(3, 100_000, {}), (1, 20_000, {}),
