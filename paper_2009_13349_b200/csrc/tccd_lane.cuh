@@ -93,6 +93,11 @@ constexpr int kLaneTailChecks = TCCD_LANE_TAIL;  // (tail handover threshold)
 #define TCCD_LANE_TAIL_WIDTH 0
 #endif
 constexpr int kLaneTailWidth = TCCD_LANE_TAIL_WIDTH;  // smallest level handed over in the tail
+#ifndef TCCD_LANE_TAIL_GRACE
+#define TCCD_LANE_TAIL_GRACE 128
+#endif
+// iterations a warp goes on after its queue ran dry before its lanes hand over
+constexpr int kLaneTailGrace = TCCD_LANE_TAIL_GRACE;
 #ifndef TCCD_LANE_CLAIM
 #define TCCD_LANE_CLAIM 32
 #endif
@@ -256,7 +261,9 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   const ColP<kLaneNT> kap{col + kColKap * kLaneNT};
   LaneEnt* const ent = reinterpret_cast<LaneEnt*>(lb);  // [2][kLaneArr]
   unsigned int* const segs = reinterpret_cast<unsigned int*>(lb + 2 * kLaneArr * 2);  // [2][kLaneSeg]
-  bool dry = false;  // (warp-uniform) this kind's queue is empty
+  // (warp-uniform) 0: this kind's queue has entries; else 1 + the iterations
+  // since it was found empty
+  int dry = 0;
   int state = 0;     // 0 idle, 2 record and coordinates in flight, 3 active
   // checks before the current level; the level's boxes (all of them, the
   // checks the reference spends on it).  (A lane query stays far below 2^31
@@ -306,12 +313,13 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   bool n_pend = false, n_have = false;
   unsigned claim_ret = 0;  // (lane 0's register)
   for (;;) {
+    dry += dry ? 1 : 0;
     if (n_pend) {
       const unsigned base = __shfl_sync(FULL, claim_ret, 0);
       const unsigned total = wq[3];
       n_pend = false;
       if (base >= total) {
-        dry = true;
+        dry = 1;
       } else {
         const unsigned nl_ = total - base < (unsigned)kLaneClaim ? total - base : (unsigned)kLaneClaim;
         wq[1] = base;
@@ -592,17 +600,22 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       const int ns = sd == 0 ? nt : (sd == 1 ? nu : nv);
       // a lattice about to leave its index range, or a level that could
       // reach the budget: the query restarts in the light tier.  A level too
-      // large for this tier is handed over to the light tier; so is, once
-      // this kind's queue is empty, the level of a query that has already
-      // run a while: the lane tier's tail (lanes idle while the last queries
-      // finish one box at a time) becomes level-parallel work for the light
-      // tier.  (kLaneTailWidth > 0 keeps narrower levels here: 8 / 16 measured
-      // no gain on 5e7 config-3 queries and doubled config 0's 1.3 ms.)  (Not a level whose first box ends the query: the lane
-      // finishes that one itself.)
+      // large for this tier is handed over to the light tier; so is,
+      // kLaneTailGrace iterations after this kind's queue was found empty, the
+      // level of a query that has already run a while: the lane tier's tail
+      // (lanes idle while the last queries finish one box at a time) becomes
+      // level-parallel work for the light tier.  About one query per lane
+      // thread is in flight when the queue runs dry, most of them with fewer
+      // than a hundred iterations to go: the grace period lets those finish
+      // here instead of arriving at the light tier in one burst (a 6.25e6-
+      // query shard: 80k -> 46k handovers, step 14.2 -> 13.5 ms).  (Not a
+      // level whose first box ends the query: the lane finishes that one
+      // itself.  kLaneTailWidth > 0 would keep narrow levels here: 8 / 16
+      // measured no gain on 5e7 config-3 queries and doubled config 0's 1.3 ms.)
       const long long m = __double_as_longlong(col[kColMc * kLaneNT]);
       if (ns > kLaneMaxSplits || nt + nu + nv > kLaneMaxLevel || Cb + nall >= m) {
         outcome = 2;
-      } else if (ncur > kLaneCap || (dry && Cb + nall >= kLaneTailChecks && ncur >= kLaneTailWidth)) {
+      } else if (ncur > kLaneCap || (dry > kLaneTailGrace && Cb + nall >= kLaneTailChecks && ncur >= kLaneTailWidth)) {
         const bool acc0 = fabs(w) < col[kColDelta * kLaneNT] || __double_as_longlong(w) < 0;
         outcome = acc0 ? outcome : 3;
       }
