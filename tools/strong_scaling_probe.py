@@ -21,7 +21,7 @@ from paper_2009_13349_b200 import workloads as W  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--queries", type=int, default=50_000_000)
-ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--out", default=None)
 args = ap.parse_args()
 w = W.generate_parallel(3, 0, args.queries)  # (before CUDA is initialised: fork)
@@ -40,15 +40,17 @@ for n in (1, 2, 4, 8):
     times = []
     for r in range(n):
         lo, hi = shard_bounds(args.queries, n, r)
-        best = None
-        for _ in range(args.reps + 1):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+        # (like bench.py: one warm-up solve, then the repetitions issued back to
+        # back between two events, so the host's launch work overlaps the GPU's)
+        solve_batch(pts[lo:hi], kind[lo:hi], outputs=(), hits=True, device=dev, raise_on_error=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.reps):
             solve_batch(pts[lo:hi], kind[lo:hi], outputs=(), hits=True, device=dev, raise_on_error=False)
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1)
-            best = ms if best is None or ms < best else best  # (first run: warm-up)
+        e1.record()
+        torch.cuda.synchronize()
+        best = e0.elapsed_time(e1) / args.reps
         times.append(round(best, 3))
     step = max(times)
     t1 = step if n == 1 else t1
