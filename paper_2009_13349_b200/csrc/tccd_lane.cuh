@@ -291,7 +291,6 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
   // its refining parents, the children of the runs before it
   unsigned nAB = 0, runAB = 0;
   int nsn = 0, run_m = 0, run_base = 0, nall_next = 0;
-  unsigned long long run = ~0ull;
   unsigned seg0 = 0, seg1 = 0;  // (the next level's first two segments)
   bool hd = false;
   static_assert(kLaneSeg == kLaneArr, "one parity offset for both tables");
@@ -401,7 +400,6 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       pk = 0; w = col[kColWb * kLaneNT];
       nAB = runAB = 0;
       nsn = run_m = run_base = nall_next = 0;
-      run = ~0ull;
       hd = false;
       state = 3;
     }
@@ -449,14 +447,6 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     };
     const int suv = nu + nv;
     const unsigned long long ti = pk >> suv;
-    // a t-split level: a new run of equal t_lo closes the previous run's
-    // segment of the next level (if it has entries)
-    const bool new_run = sd == 0 && ti != run;
-    close_segment(new_run && runAB != 0);
-    run_base += new_run ? 2 * run_m : 0;
-    run_m = new_run ? 0 : run_m;
-    runAB = new_run ? 0u : runAB;
-    run = sd == 0 ? ti : run;
     const double wt = lane_pow2(xt - nt), wu = lane_pow2(1023 - nu), wv = lane_pow2(1023 - nv);
     const double t0 = (double)ti * wt;
     const double u0 = (double)((pk >> nv) & ((1ull << nu) - 1ull)) * wu;
@@ -549,9 +539,17 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     k += go ? 1 : 0;
     pk = go ? nx.x : pk;
     w = go ? __longlong_as_double((long long)nx.y) : w;
-    // ---- level end
+    // ---- level end; in a t-split level, the end of a run of equal t_lo (the
+    // next entry, already loaded, starts another): either closes the run's
+    // segment of the next level, if it has entries
     const bool lvl_end = go && k == ncur;
-    close_segment(lvl_end && runAB != 0);
+    {
+      const bool run_end = lvl_end || (go && sd == 0 && (pk >> suv) != ti);
+      close_segment(run_end && runAB != 0);
+      run_base += run_end ? 2 * run_m : 0;
+      run_m = run_end ? 0 : run_m;
+      runAB = run_end ? 0u : runAB;
+    }
     const int nnext = (int)((nAB & 0xffffu) + (nAB >> 16));
     if (lvl_end && nnext == 0) {
       const long long m = __double_as_longlong(col[kColMc * kLaneNT]);
@@ -592,7 +590,6 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       sn = seg1;
       nAB = runAB = 0u;
       nsn = run_m = run_base = nall_next = 0;
-      run = ~0ull;
       // every refining box of the level split along sd
       nt += sd == 0 ? 1 : 0;
       nu += sd == 1 ? 1 : 0;
