@@ -173,11 +173,7 @@ __device__ __forceinline__ void load_params(const Args& a, long long q, QueryPar
 
 }  // namespace tccd
 
-#ifdef TCCD_LANE_BOXWISE
-#include "tccd_lane_boxwise.cuh"  // (round-2 first lane tier: one box per iteration; A/B timing only)
-#else
 #include "tccd_lane.cuh"
-#endif
 
 namespace tccd {
 
@@ -666,7 +662,9 @@ int configure_lane() {
   static bool done[256] = {};
   const int dev = current_device();
   if (dev >= 0 && dev < 256 && done[dev]) return TCCD_OK;
-  if (cudaFuncSetAttribute(lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(lane_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kLaneSmemBytes) != cudaSuccess ||
+      cudaFuncSetAttribute(lane_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)kLaneSmemBytes) != cudaSuccess)
     return TCCD_E_CUDA;
   if (dev >= 0 && dev < 256) done[dev] = true;
@@ -923,7 +921,9 @@ int tccd_solve_batch(const tccd_batch* b_in, void* stream) {
     if (mark(TCCD_STAGE_PROLOGUE) != cudaSuccess) return TCCD_E_CUDA;
     if (lanes) {
       if (configure_lane() != TCCD_OK) return TCCD_E_CUDA;
-      lane_kernel<<<L.lane_blocks, kLaneNT, kLaneSmemBytes, st>>>(a, lio);
+      // (every query of the call at separation 0: the hull is compared as is)
+      if (!a.sep && a.sep_all == 0.0) lane_kernel<true><<<L.lane_blocks, kLaneNT, kLaneSmemBytes, st>>>(a, lio);
+      else lane_kernel<false><<<L.lane_blocks, kLaneNT, kLaneSmemBytes, st>>>(a, lio);
       ++launches;
       if (cudaGetLastError() != cudaSuccess || mark(TCCD_STAGE_LANE) != cudaSuccess)
         return TCCD_E_CUDA;

@@ -191,7 +191,9 @@ __device__ __forceinline__ int classify_full(PtrT P, const Box& b, EpsT eps, dou
 // two independent evaluations a thread interleaves axis by axis (the lane
 // tier classifies children when their parent is refined).  Each box sees
 // exactly classify_full's operations.
-template <int KIND, typename PtrT, typename EpsT>
+// (SEP0: the whole call has separation 0 -- the hull is compared as is: x -
+// 0 and x + 0 change no comparison.)
+template <int KIND, bool SEP0, typename PtrT, typename EpsT>
 __device__ __forceinline__ void classify_pair(PtrT P, const Box& a, const Box& b, EpsT eps,
                                               double sep, int& cls_a, double& wb_a, int& cls_b,
                                               double& wb_b) {
@@ -229,7 +231,8 @@ __device__ __forceinline__ void classify_pair(PtrT P, const Box& a, const Box& b
     hull_axis<KIND, true>(P, ax, b.t0, b_omt0, b.t1, b_omt1, wb, mnb, mxb);
 #endif
     const double e = eps[ax];
-    const double loa = mna - sep, hia = mxa + sep, lob = mnb - sep, hib = mxb + sep;
+    const double loa = SEP0 ? mna : mna - sep, hia = SEP0 ? mxa : mxa + sep;
+    const double lob = SEP0 ? mnb : mnb - sep, hib = SEP0 ? mxb : mxb + sep;
     dis_a |= loa > e || hia < -e;
     dis_b |= lob > e || hib < -e;
     con_a &= loa >= -e && hia <= e;

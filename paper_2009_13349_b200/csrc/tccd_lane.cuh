@@ -250,7 +250,9 @@ __device__ __forceinline__ void lane_flush(const LaneIO& io, unsigned* si, int k
 __device__ __forceinline__ double lane_pow2(int x) { return __hiloint2double(x << 20, 0); }
 
 // One kind's queue (kind is warp-uniform; only the classification is
-// specialized on it, so the loop's code exists once).
+// specialized on it, so the loop's code exists once).  SEP0: the call's
+// separation is 0 for every query.
+template <bool SEP0>
 __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, double* col,
                                           unsigned* si_, unsigned* wq, long long* sq,
                                           unsigned long long* lb, const int kind) {
@@ -496,9 +498,9 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     double wa_, wb_;
     int ca, cbx;
     {
-      const double sep = col[kColSep * kLaneNT];
-      if (kind == 0) classify_pair<0>(P, ba, bb, eps, sep, ca, wa_, cbx, wb_);
-      else classify_pair<1>(P, ba, bb, eps, sep, ca, wa_, cbx, wb_);
+      const double sep = SEP0 ? 0.0 : col[kColSep * kLaneNT];
+      if (kind == 0) classify_pair<0, SEP0>(P, ba, bb, eps, sep, ca, wa_, cbx, wb_);
+      else classify_pair<1, SEP0>(P, ba, bb, eps, sep, ca, wa_, cbx, wb_);
     }
     const bool na = refine && ca != kDisjoint;
     const bool nb = refine && push_hi && cbx != kDisjoint;
@@ -684,6 +686,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
 constexpr size_t kLaneSmemBytes = (size_t)kLaneCol * kLaneNT * 8 + (size_t)kLaneInt * kLaneNT * 4 +
                                   (size_t)(kLaneNT / 32) * (2 * kLaneClaim * 8 + 4 * 4);
 
+template <bool SEP0>
 __global__ void __launch_bounds__(kLaneNT, TCCD_NMINB) lane_kernel(Args a, LaneIO io) {
   extern __shared__ __align__(16) unsigned char lane_smem[];
   double* const Ps = reinterpret_cast<double*>(lane_smem);
@@ -702,7 +705,7 @@ __global__ void __launch_bounds__(kLaneNT, TCCD_NMINB) lane_kernel(Args a, LaneI
   const long long gw = gt >> 5, nw = (long long)gridDim.x * (kLaneNT / 32);
   int kind = (nvf + nee) > 0 && (unsigned long long)gw * (nvf + nee) < nee * (unsigned long long)nw;
   for (int pass = 0; pass < 2; ++pass, kind ^= 1)
-    lane_loop(a, io, col, si, Sw + 4 * (threadIdx.x >> 5),
+    lane_loop<SEP0>(a, io, col, si, Sw + 4 * (threadIdx.x >> 5),
               Sq + (threadIdx.x >> 5) * 2 * kLaneClaim, lb, kind);
 }
 
