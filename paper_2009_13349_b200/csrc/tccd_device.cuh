@@ -13,6 +13,19 @@
 
 namespace tccd {
 
+// Bounds checks of a diagnostic build (-DTCCD_CHECKS): a violated index
+// traps the kernel (the launch fails with an error) instead of corrupting
+// memory.  Compiled out otherwise.
+#ifdef TCCD_CHECKS
+#define TCCD_ASSERT(c) \
+  do {                 \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define TCCD_ASSERT(c) \
+  do {                 \
+  } while (0)
+#endif
 constexpr int kDisjoint = 0;    // _kernel.py:36
 constexpr int kIntersects = 1;  // _kernel.py:37
 constexpr int kContained = 2;   // _kernel.py:38

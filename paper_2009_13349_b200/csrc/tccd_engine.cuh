@@ -46,19 +46,6 @@ namespace tccd {
 
 constexpr int kIntMax = 0x7fffffff;
 
-// Bounds checks of a diagnostic build (-DTCCD_CHECKS): a violated index
-// traps the kernel (the launch fails with an error) instead of corrupting
-// memory.  Compiled out otherwise.
-#ifdef TCCD_CHECKS
-#define TCCD_ASSERT(c) \
-  do {                 \
-    if (!(c)) __trap(); \
-  } while (0)
-#else
-#define TCCD_ASSERT(c) \
-  do {                 \
-  } while (0)
-#endif
 constexpr uint8_t kClassified = 64;  // flag bit: box already classified
 constexpr uint8_t kHead = 128;       // flag bit: first box of a run of equal t_lo
 // P4c modes of a slot: children kept here (closed form), level carried

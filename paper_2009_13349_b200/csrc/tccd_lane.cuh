@@ -430,6 +430,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       // and straight into the registers that carry it to the next
       // iteration: a predicated load went through temporaries that were
       // copied, and waited for, right behind it)
+      TCCD_ASSERT(!more || (posn >= 0 && posn < kLaneArr));
       nx = *reinterpret_cast<const ulonglong2*>(cur + (more ? posn : 0));
     }
     // closing a segment of the next level; its first one fixes the level's
@@ -438,6 +439,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
     // parent's index; the run's lower children, one per refining parent,
     // come before it)
     auto close_segment = [&](bool close) {
+      TCCD_ASSERT(!close || nsn < kLaneSeg);
       if (close) snx[nsn] = runAB;
       if (close && nsn == 0) {
         seg0 = runAB;
@@ -511,6 +513,10 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
       const double eb = cbx == kContained ? -wb_ : wb_;
       const int nA = (int)(nAB & 0xffffu), nB = (int)(nAB >> 16);
       const int posb = sd == 0 ? kLaneArr - 1 - nB : nA + (na ? 1 : 0);
+      // (bottom and top parts never meet: a level of <= kLaneCap boxes has <=
+      // kLaneArr children)
+      TCCD_ASSERT(!(na || nb) || (ncur <= kLaneCap && nA + nB + (na ? 1 : 0) + (nb ? 1 : 0) <= kLaneArr));
+      TCCD_ASSERT(!nb || (posb >= 0 && posb < kLaneArr));
       if (na) nxt[nA] = LaneEnt{lo, ea};
       if (nb) nxt[posb] = LaneEnt{hi, eb};
       const unsigned add = (na ? 1u : 0u) + (nb ? (sd == 0 ? 0x10000u : 1u) : 0u);
@@ -646,6 +652,7 @@ __device__ __forceinline__ void lane_loop(const Args& a, const LaneIO& io, doubl
             const int ca_ = (int)(sg & 0xffffu), cb_ = (int)(sg >> 16);
             for (int i = 0; i < ca_ + cb_; ++i, ++j) {
               const int p = i < ca_ ? qa++ : qb--;
+              TCCD_ASSERT(p >= 0 && p < kLaneArr && j < ncur);
               const Box bx = lane_box(cw[p].pk, nt, nu, nv, t_max);
               io.pbox[off + j] = bx;
               io.pflag[off + j] = (uint8_t)(j == 0 || bx.t0 != prev ? 128 : 0);  // the engine's kHead

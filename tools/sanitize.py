@@ -10,8 +10,8 @@ by the engine asserted against its array's capacity; a violation traps):
 or under compute-sanitizer where it is available (memcheck, racecheck with
 --quick).
 
-Covers: prologue, light / medium / giant engine tiers (mixed batch; giant
-alone), the general (non-dyadic t_max) ordering path, minimum separation,
+Covers: prologue, lane tier, light / medium / giant engine tiers (mixed
+batch; giant alone), the general (non-dyadic t_max) ordering path, minimum separation,
 per-query delta / max_checks, the IRF baseline's three passes and the GPU
 broad phase.  Every solver result is checked bit for bit against the oracle
 (test infrastructure), so a run that exits 0 is also a parity pass.
@@ -67,6 +67,7 @@ def main():
         ref = oracle.solve_batch(w.points, w.kind, d, m, w.separation, tm)
         same(got, ref, what)
 
+    run(3, 0, 8192 // s, "config 3 (lane tier, handovers)")
     run(1, 0, 2048 // s, "config 1 (light / medium / giant)")
     run(0, 5000, 1024 // s, "config 0")
     run(2, 0, 256 // s, "config 2 (per-query delta / max_checks)")
