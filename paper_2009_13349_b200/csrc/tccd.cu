@@ -247,11 +247,16 @@ __global__ void __launch_bounds__(kPrologueThreads, TCCD_PRO_MINB) prologue_kern
       const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + i);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + i) : "memory");
     }
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
 #endif
   }
-  __syncthreads();
+  // (the per-query parameters are loaded while the tile is in flight)
   const int t = threadIdx.x;
+  QueryParams qp;
+  if (t < nb) load_params(a, base + t, qp);
+#ifndef TCCD_PRO_SYNC_LOAD
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+#endif
+  __syncthreads();
   bool survive = false;
   int lane_kind = -1;  // survivor routed to the lane tier (its kind)
   Pre pre;
@@ -259,8 +264,6 @@ __global__ void __launch_bounds__(kPrologueThreads, TCCD_PRO_MINB) prologue_kern
   if (t < nb) {
     const long long q = base + t;
     const double* P = tile + 24 * t;
-    QueryParams qp;
-    load_params(a, q, qp);
     uint8_t st = kHit;
     if (!params_valid(qp.kind, qp.delta, qp.max_checks, qp.sep, qp.t_max) ||
         qp.max_checks > a.max_checks_max) {
